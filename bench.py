@@ -1,0 +1,488 @@
+#!/usr/bin/env python
+"""bench.py — corr-lookup ms/iter + peak HBM at 8K (L=4, r=4, D=256) vs roofline.
+
+One step = one full lookup run of an image pair through the partial sampler:
+fmap2 pyramid + init_state + 12 per-iteration `__call__(coords)` lookups
+(BASELINE.json config 4: 540x960 features, D=256, L=4, r=4, 12 iterations).
+Inputs are resident in HBM for `value`; `e2e` repeats the step through the
+public API from pinned host buffers with every H2D/D2H inside the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {b200,reference}]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (query-row bands)
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+# name: (H, W, D, radius, levels, iterations, normalize)
+CONFIGS = {
+    "C1": (46, 62, 256, 4, 4, 12, False),
+    "C2": (135, 240, 256, 4, 4, 32, False),
+    "C3": (270, 480, 256, 4, 4, 12, True),
+    "C4": (540, 960, 256, 4, 4, 12, False),
+}
+METRIC = "corr-lookup ms/iter + peak HBM at 8K (L=4,r=4,D=256) at 1/2/4/8 B200 vs roofline"
+FP32_LANES_PER_SM = 128
+N_SMS = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="C4")
+    ap.add_argument("--variant", choices=["partial", "ondemand", "dense"], default="partial")
+    ap.add_argument("--strict", action="store_true", help="reference-exact arithmetic")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-compare", action="store_true")
+    ap.add_argument("--profile-only", action="store_true",
+                    help="run warmup+steps only (for ncu); print nothing else")
+    ap.add_argument("--cpu-baseline-worker", default=None, help=argparse.SUPPRESS)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref = the unmodified corrvol package, cython lane)
+# ---------------------------------------------------------------------------
+
+_REF_SC = None
+
+
+def _ref_band_job(args):
+    """Reference partial sampler (B=8) on rows [a, b) of the scenario; returns
+    (t_prep_s, t_iters_s).  Runs in a forked worker, single-threaded."""
+    a, b = args
+    cv, sc = _REF_SC
+    f1 = cv.FeatureMap(values=sc.f1[a:b])
+    f2 = cv.FeatureMap(values=sc.f2)
+    t0 = time.perf_counter()
+    st = cv.init_state(f1, f2, cv.LookupSpec(*sc.spec_args), 8, backend="cython")
+    t1 = time.perf_counter()
+    for c in sc.centroid_fields:
+        cv.sample_iteration(st, cv.CentroidField(coords=c[a:b].astype(np.float64)))
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1
+
+
+class _RefScenario:
+    def __init__(self, cfg):
+        from paper_2505_16942_b200.scenario import gen_scenario
+        from paper_2505_16942_b200.types import LookupSpec
+
+        h, w, d, r, levels, n_iter, norm = CONFIGS[cfg]
+        sc = gen_scenario(0, (h, w, d), n_iter, LookupSpec(r, levels, norm),
+                          coords_dtype=np.float32)
+        self.f1, self.f2, self.centroid_fields = sc.f1, sc.f2, sc.centroid_fields
+        self.spec_args = (r, levels, norm)
+        self.h, self.w, self.iters = h, w, n_iter
+
+
+def reference_sample(cfg: str, workers: int, rows_per_worker: int):
+    """Time the reference on `workers` parallel row bands; extrapolate to the frame.
+
+    The reference hot path is single-threaded (numpy + GIL-held Cython,
+    _ckernels.pyx:1), so the all-cores figure runs one process per core on
+    disjoint row bands.  Frame time on `workers` cores =
+    prep (fmap2 pyramid + patch-major, once per core) + per-band iteration time
+    x frame_rows / (rows_per_worker * workers).
+    """
+    global _REF_SC
+    from oracle import import_reference
+
+    cv = import_reference()
+    if cv is None:
+        raise RuntimeError("oracle/_ref not built")
+    if _REF_SC is None:
+        _REF_SC = (cv, _RefScenario(cfg))
+    sc = _REF_SC[1]
+    start = (sc.h // 2) // 8 * 8
+    bands = [(start + i * rows_per_worker, start + (i + 1) * rows_per_worker)
+             for i in range(workers)]
+    bands = [(a % sc.h // 8 * 8, min(a % sc.h // 8 * 8 + rows_per_worker, sc.h)) for a, _ in bands]
+    t0 = time.perf_counter()
+    if workers == 1:
+        res = [_ref_band_job(bands[0])]
+    else:
+        ctx = mp.get_context("fork")
+        with ctx.Pool(workers) as pool:
+            res = pool.map(_ref_band_job, bands)
+    wall = time.perf_counter() - t0
+    prep = statistics.mean(r[0] for r in res)
+    iters = statistics.mean(r[1] for r in res)
+    rows_done = rows_per_worker * workers
+    frame_s = prep + iters * sc.h / rows_done
+    return {"ms_per_iter": 1e3 * frame_s / sc.iters, "frame_s": frame_s, "wall_s": wall,
+            "prep_s": prep, "iters_s_per_band": iters, "bands": bands, "cores": workers,
+            "iterations": sc.iters}
+
+
+def cpu_baseline_worker(cfg: str) -> None:
+    out = reference_sample(cfg, 1, 32)
+    print(json.dumps(out))
+
+
+def run_reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    h, w, d, r, levels, n_iter, norm = CONFIGS[args.config]
+    times = []
+    for i in range(args.warmup + args.steps):
+        res = reference_sample(args.config, cores, 8)
+        if i >= args.warmup:
+            times.append(res["ms_per_iter"])
+    v = statistics.mean(times)
+    sample = (f"reference corrvol 0.1.0 partial sampler (B=8, cython lane), {cores} processes x "
+              f"8-row bands of {args.config} ({h}x{w}, D={d}, L={levels}, r={r}), "
+              f"{n_iter} iterations each, extrapolated linearly in rows to the full frame")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms/iter",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(v * n_iter, 3), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config} {h}x{w} D={d} L={levels} r={r} "
+                               f"{n_iter} iterations", "parallelism": f"{cores} CPU processes"},
+        "cpu_baseline": {"value": round(v, 3), "unit": "ms/iter", "cores": cores,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": round(v, 3), "unit": "ms/iter", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.file = None
+
+    def start(self):
+        try:
+            self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.file, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.file.flush()
+        rows = [l.split(",") for l in Path(self.file.name).read_text().splitlines() if l.strip()]
+        os.unlink(self.file.name)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for row in rows:
+            try:
+                sm.append(float(row[1]))
+                smax = float(row[2])
+                for nm, v in zip(names, row[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    if args.cpu_baseline_worker:
+        cpu_baseline_worker(args.cpu_baseline_worker)
+        return
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_16942_b200 as cvb
+    from paper_2505_16942_b200 import _lib
+    from paper_2505_16942_b200.parallel import row_bands
+    from paper_2505_16942_b200.sparse import sample_iteration_timed
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allmax(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    h, w, d, r, levels, n_iter, norm = CONFIGS[args.config]
+    spec = cvb.LookupSpec(r, levels, norm)
+    sc = cvb.gen_scenario(0, (h, w, d), n_iter, spec, coords_dtype=np.float32)
+    a, b = row_bands(h, world)[rank]
+    rows = b - a
+    f1_host = torch.from_numpy(np.ascontiguousarray(sc.f1[a:b]))
+    f2_host = torch.from_numpy(sc.f2)
+    co_host = [torch.from_numpy(np.ascontiguousarray(c[a:b])) for c in sc.centroid_fields]
+    f1_dev = f1_host.to(dev)
+    f2_dev = f2_host.to(dev)
+    co_dev = [c.to(dev) for c in co_host]
+    k1 = spec.window
+    out = torch.empty((rows, w, levels, k1, k1), dtype=torch.float32, device=dev)
+    cents = [cvb.CentroidField(c, check=False) for c in co_dev]
+
+    def step(variant=args.variant, cache=True):
+        s = cvb.CorrSampler(cvb.FeatureMap(f1_dev, check=False),
+                            cvb.FeatureMap(f2_dev, check=False), spec, variant=variant,
+                            strict=args.strict, cache=cache, check=False)
+        for c in cents:
+            s(c, out=out)
+        return s
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        return allmax(e0.elapsed_time(e1) / steps)
+
+    if args.profile_only:
+        timed(step, args.steps, args.warmup)
+        return
+
+    # ---- main measurement: inputs resident in HBM -------------------------
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats(dev)
+    base_alloc = torch.cuda.memory_allocated(dev)
+    clocks = Clocks(local).start()
+    launches0 = _lib.launch_count()
+    ms_step = timed(step, args.steps, 0)
+    launches = _lib.launch_count() - launches0
+    clk = clocks.stop()
+    peak_bytes = int(allmax(torch.cuda.max_memory_allocated(dev)))
+    ms_iter = ms_step / n_iter
+    p_total = h * w
+    lookups_s = p_total * n_iter / (ms_step / 1e3)
+
+    # ---- per-kernel timing (tile mode): contraction vs gather/sampler -----
+    kern = {}
+    if args.variant == "partial":
+        st = cvb.init_state(cvb.FeatureMap(f1_dev, check=False), cvb.FeatureMap(f2_dev, check=False),
+                            spec, strict=args.strict)
+        evs = [sample_iteration_timed(st, c, out) for c in cents]
+        torch.cuda.synchronize()
+        t_con = [e[0].elapsed_time(e[1]) for e in evs]
+        t_gat = [e[1].elapsed_time(e[2]) for e in evs]
+        kern = {"contract_ms": t_con, "gather_ms": t_gat,
+                "device_counters": st.device_counters}
+        del st
+
+    # ---- roofline ----------------------------------------------------------
+    peaks_path = ROOT / "MEASURED_PEAKS.json"
+    peaks = json.loads(peaks_path.read_text()) if peaks_path.exists() else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    geom_path = ROOT / "profiles" / f"geometry_{args.config}.json"
+    geom = json.loads(geom_path.read_text()) if geom_path.exists() else None
+    out_bytes_iter = rows * w * levels * k1 * k1 * 4
+    coord_bytes_iter = rows * w * 2 * 4
+    roofline = None
+    secondary = None
+    if kern:
+        tc, tg = sum(kern["contract_ms"]), sum(kern["gather_ms"])
+        gather_bytes = (out_bytes_iter + coord_bytes_iter) * n_iter
+        gather_gbs = gather_bytes / (tg / 1e3) / 1e9
+        r_gather = {"kernel": "partial_sample_kernel (gather/bilinear sampler)", "bound": "hbm",
+                    "achieved": round(gather_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(gather_gbs / hbm_peak, 4), "traffic": None,
+                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})",
+                    "alg_bytes_per_launch": gather_bytes / n_iter,
+                    "avg_launch_ms": tg / n_iter, "share_of_step": round(tg / (tc + tg), 3)}
+        fp32_peak = N_SMS * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
+        r_con = None
+        if geom is not None and world == 1:
+            flops = geom["flops_alg_run"]
+            tf = flops / (tc / 1e3) / 1e12
+            r_con = {"kernel": "partial_contract_kernel (tiler + incremental contraction)",
+                     "bound": "fp32", "achieved": round(tf, 2), "peak": round(fp32_peak, 1),
+                     "unit": "TFLOP/s", "frac": round(tf / fp32_peak, 4), "traffic": None,
+                     "peak_source": "FFMA nominal 148 SM x 128 lanes x 2 x sm_max_mhz "
+                                    "(no measured FP32 peak; MEASURED_PEAKS has HBM/bf16 only)",
+                     "alg_flops_per_launch": flops / n_iter, "avg_launch_ms": tc / n_iter,
+                     "share_of_step": round(tc / (tc + tg), 3),
+                     "executed_flops": 2 * d * kern["device_counters"]["dots"]}
+        if r_con is not None and tc >= tg:
+            roofline, secondary = r_con, r_gather
+        else:
+            roofline, secondary = r_gather, r_con
+
+    # ---- run-level roofline ---------------------------------
+    pyr_bytes = sum((h >> l) * (w >> l) for l in range(1, levels)) * d * 4
+    bytes_alg = n_iter * (out_bytes_iter + coord_bytes_iter) * world + h * w * d * 8 + 2 * pyr_bytes
+    run_floor_ms = bytes_alg / (hbm_peak * 1e9) * 1e3
+
+    # ---- comparisons in the same build (N=1) --------------------------------
+    compare = {}
+    dense_bytes = cvb.estimate_dense_bytes((h, w), (h, w), levels)
+    if not args.no_compare and world == 1:
+        compare["ondemand_ms_per_iter"] = round(timed(lambda: step("ondemand"), 1, 1) / n_iter, 3)
+        compare["partial_nocache_ms_per_iter"] = round(
+            timed(lambda: step("partial", cache=False), 1, 1) / n_iter, 3)
+        free, _ = torch.cuda.mem_get_info(dev)
+        if dense_bytes < 0.85 * free:
+            compare["dense_ms_per_iter"] = round(timed(lambda: step("dense"), 1, 1) / n_iter, 3)
+        else:
+            compare["dense"] = {"oom": True, "bytes": dense_bytes, "free_bytes": free}
+    torch.cuda.synchronize()
+
+    # ---- e2e: public API from pinned host buffers ---------------------------
+    e2e = None
+    if not args.no_e2e:
+        f1_pin = f1_host.pin_memory()
+        f2_pin = f2_host.pin_memory()
+        co_pin = [c.pin_memory() for c in co_host]
+        outs_pin = [torch.empty(out.shape, dtype=torch.float32).pin_memory() for _ in range(2)]
+        copy_stream = torch.cuda.Stream(dev)
+
+        def e2e_step():
+            f1d = f1_pin.to(dev, non_blocking=True)
+            f2d = f2_pin.to(dev, non_blocking=True)
+            s = cvb.CorrSampler(cvb.FeatureMap(f1d, check=False), cvb.FeatureMap(f2d, check=False),
+                                spec, variant=args.variant, strict=args.strict, check=False)
+            bufs = [torch.empty_like(out), torch.empty_like(out)]
+            done = [None, None]
+            for i, c in enumerate(co_pin):
+                j = i % 2
+                if done[j] is not None:
+                    torch.cuda.current_stream().wait_event(done[j])
+                res = s(cvb.CentroidField(c.to(dev, non_blocking=True), check=False), out=bufs[j])
+                ev = torch.cuda.Event()
+                ev.record()
+                with torch.cuda.stream(copy_stream):
+                    copy_stream.wait_event(ev)
+                    outs_pin[j].copy_(res.values, non_blocking=True)
+                    done[j] = torch.cuda.Event()
+                    done[j].record(copy_stream)
+            torch.cuda.current_stream().wait_stream(copy_stream)
+
+        e2e_steps = max(1, min(args.steps, 3))
+        ms_e2e = timed(e2e_step, e2e_steps, 1)
+        e2e = {"value": round(ms_e2e / n_iter, 3), "unit": "ms/iter",
+               "h2d_bytes_per_step": (f1_host.numel() + f2_host.numel()) * 4 +
+               sum(c.numel() * 4 for c in co_host),
+               "d2h_bytes_per_step": out.numel() * 4 * n_iter,
+               "steps": e2e_steps,
+               "note": "CorrSampler from pinned host fmaps; per iteration coords H2D + "
+                       "lookup + full cost-map D2H (double-buffered copy stream)"}
+
+    # ---- CPU baseline (rank 0, N=1) ----------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            res = subprocess.run(["taskset", "-c", "0", sys.executable, str(ROOT / "bench.py"),
+                                  "--cpu-baseline-worker", args.config],
+                                 capture_output=True, text=True, timeout=600)
+            ref = json.loads(res.stdout.strip().splitlines()[-1])
+            cpu = {"value": round(ref["ms_per_iter"], 3), "unit": "ms/iter", "cores": 1,
+                   "kind": "reference",
+                   "sample": f"reference corrvol 0.1.0 partial sampler (B=8, cython lane) on "
+                             f"rows {ref['bands'][0][0]}..{ref['bands'][0][1]} of {args.config}, "
+                             f"{ref['iterations']} iterations, 1 core (taskset -c 0); prep "
+                             f"{ref['prep_s']:.1f}s + band iterations {ref['iters_s_per_band']:.1f}s "
+                             f"extrapolated linearly in rows to the full frame"}
+        except Exception as exc:  # report, never fake
+            cpu = {"value": None, "unit": "ms/iter", "cores": 1, "kind": "reference",
+                   "sample": f"failed: {type(exc).__name__}: {exc}"[:300]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(ms_iter, 4), "unit": "ms/iter",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 3), "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded N(0,1) fmaps, Gaussian-smoothed flow drift; "
+                    "gen_scenario recipe, fp32 centroids)",
+            "config": {"workload": f"{args.config} {h}x{w} features D={d} L={levels} r={r} "
+                                   f"{n_iter} iterations, one image pair per step",
+                       "variant": args.variant, "arith": "strict" if args.strict else "fast",
+                       "parallelism": f"query-row bands x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (fmaps 2x531 MB, cache GBs)"},
+            "lookups_per_s": round(lookups_s, 1),
+            "peak_hbm_bytes": peak_bytes,
+            "peak_hbm_bytes_over_inputs": peak_bytes - base_alloc if world == 1 else None,
+            "dense_bytes": dense_bytes,
+            "memory_reduction_vs_dense": round(1 - peak_bytes / dense_bytes, 5),
+            "roofline": roofline, "roofline_secondary": secondary,
+            "run_roofline": {"bytes_alg": bytes_alg, "floor_ms_per_step": round(run_floor_ms, 4),
+                             "frac": round(run_floor_ms / ms_step, 4),
+                             "flops_alg": geom["flops_alg_run"] if geom else None},
+            "kernel_ms": {k: [round(x, 4) for x in v] for k, v in kern.items()
+                          if k.endswith("_ms")} if kern else None,
+            "device_counters": kern.get("device_counters") if kern else None,
+            "compare": compare or None,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

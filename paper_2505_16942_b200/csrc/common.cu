@@ -1,0 +1,41 @@
+// Library plumbing: error strings, launch accounting, version.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <atomic>
+
+#include "common.cuh"
+
+namespace cvb {
+
+static thread_local char g_err[512] = "";
+static std::atomic<unsigned long long> g_launches{0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int check_launch(const char* what) {
+  note_launch();
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return CVB_ERR_CUDA;
+  }
+  return CVB_OK;
+}
+
+}  // namespace cvb
+
+extern "C" {
+
+int cvb_abi_version(void) { return CVB_ABI_VERSION; }
+const char* cvb_last_error(void) { return cvb::g_err; }
+unsigned long long cvb_launch_count(void) { return cvb::g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+"""CorrSampler: the per-iteration `__call__(coords)` lookup with a variant switch.
+
+The reference has no class API (its harness calls the three samplers
+directly, harness.py:36,190-274,459-471); RAFT/SEA-RAFT callers use a
+`CorrBlock(fmap1, fmap2)(coords)` object.  CorrSampler provides that shape on
+top of the reference-named functions:
+
+    sampler = CorrSampler(fmap1, fmap2, LookupSpec(4, 4), variant="partial")
+    for it in range(iters):
+        costs = sampler(coords)          # [H, W, L, 2r+1, 2r+1] on the GPU
+
+variant: "partial" (sparse.py, the north-star path), "ondemand"
+(ondemand.py), "dense" (dense.py; raises MemoryError when the volume would
+not fit, the analogue of the reference bench's oom row, harness.py:330-333).
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+
+from .dense import build_feature_pyramid, build_volume_pyramid, estimate_dense_bytes, lookup_dense
+from .ondemand import lookup_on_demand
+from .sparse import init_state, memory_footprint, sample_iteration
+from .types import CentroidField, CostMaps, FeatureMap, LookupSpec
+
+VARIANTS = ("dense", "ondemand", "partial")
+_ALIASES = {"sparse": "partial"}
+
+
+class CorrSampler:
+    def __init__(self, fmap1, fmap2, spec: LookupSpec, variant: str = "partial", block: int = 8,
+                 cache: bool = True, strict: bool = False, mode: str = "tile",
+                 dense_mode: str = "pool_features", dense_limit_bytes: Optional[int] = None,
+                 check: bool = True, **state_kwargs):
+        variant = _ALIASES.get(variant, variant)
+        if variant not in VARIANTS:
+            raise ValueError(f"variant must be one of {VARIANTS}, got {variant!r}")
+        self.variant = variant
+        self.spec = spec
+        self.strict = strict
+        self.f1 = fmap1 if isinstance(fmap1, FeatureMap) else FeatureMap(fmap1, check=check)
+        self.f2 = fmap2 if isinstance(fmap2, FeatureMap) else FeatureMap(fmap2, check=check)
+        self.check = check
+        self.state = None
+        self.volume = None
+        self.pyramid = None
+        if variant == "partial":
+            self.state = init_state(self.f1, self.f2, spec, block, cache_enabled=cache,
+                                    mode=mode, strict=strict, **state_kwargs)
+            self.pyramid = self.state.pyramid
+        elif variant == "ondemand":
+            self.pyramid = build_feature_pyramid(self.f2, spec.levels)
+        else:
+            need = estimate_dense_bytes((self.f1.height, self.f1.width),
+                                        (self.f2.height, self.f2.width), spec.levels)
+            limit = dense_limit_bytes
+            if limit is None:
+                free, _ = torch.cuda.mem_get_info(self.f1.values.device)
+                limit = int(free * 0.9)
+            if need > limit:
+                raise MemoryError(f"dense volume needs {need} bytes (> limit {limit})")
+            self.volume = build_volume_pyramid(self.f1, self.f2, spec.levels, mode=dense_mode,
+                                               strict=strict)
+
+    def __call__(self, coords, out: Optional[torch.Tensor] = None) -> CostMaps:
+        cents = coords if isinstance(coords, CentroidField) else CentroidField(coords,
+                                                                                check=self.check)
+        if self.variant == "partial":
+            return sample_iteration(self.state, cents, out=out)
+        if self.variant == "ondemand":
+            return lookup_on_demand(self.f1, self.pyramid, cents, self.spec, strict=self.strict,
+                                    out=out)
+        return lookup_dense(self.volume, cents, self.spec, strict=self.strict, out=out)
+
+    def memory_bytes(self) -> int:
+        """Analytic bytes the variant holds between iterations."""
+        feats = self.f1.values.numel() * 4
+        if self.variant == "partial":
+            return memory_footprint(self.state)["total_bytes"]
+        feats += sum(l.values.numel() * 4 for l in self.pyramid.levels) if self.pyramid else 0
+        if self.variant == "dense":
+            return self.volume.nbytes() + self.f1.values.numel() * 4 + \
+                self.f2.values.numel() * 4
+        return feats
