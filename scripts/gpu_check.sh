@@ -1,5 +1,5 @@
 set -x
-cd $GRAFT_REPO_ROOT
+cd ${GRAFT_REPO_ROOT:-.}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke1.log 2>&1; echo smoke rc $?
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu1.log 2>&1; echo pytest rc $?
