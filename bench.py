@@ -330,7 +330,7 @@ def main():
         t_con = [e[0].elapsed_time(e[1]) for e in evs]
         t_gat = [e[1].elapsed_time(e[2]) for e in evs]
         kern = {"contract_ms": t_con, "gather_ms": t_gat,
-                "device_counters": st.device_counters}
+                "device_counters": st.device_counters, "tensor_cores": st.tc}
         del st
 
     # ---- roofline ----------------------------------------------------------
@@ -360,14 +360,29 @@ def main():
         if geom is not None and world == 1:
             flops = geom["flops_alg_run"]
             tf = flops / (tc / 1e3) / 1e12
-            r_con = {"kernel": "partial_contract_kernel (tiler + incremental contraction)",
-                     "bound": "fp32", "achieved": round(tf, 2), "peak": round(fp32_peak, 1),
-                     "unit": "TFLOP/s", "frac": round(tf / fp32_peak, 4), "traffic": None,
-                     "peak_source": "FFMA nominal 148 SM x 128 lanes x 2 x sm_max_mhz "
-                                    "(no measured FP32 peak; MEASURED_PEAKS has HBM/bf16 only)",
+            if kern["tensor_cores"]:
+                peak = peaks.get("bf16_tflops_sustained", 1400.0)
+                src = ("MEASURED_PEAKS.json bf16_tflops_sustained (kind::f16 dense rate; "
+                       "kernel timed inside the step)" if "bf16_tflops_sustained" in peaks
+                       else "fallback 1.4 PFLOP/s sustained")
+                name = "partial_contract_tc_kernel (tiler + incremental tcgen05 contraction)"
+                bound = "tensor"
+                executed = 3 * 2 * d * kern["device_counters"]["dots"]
+            else:
+                peak = fp32_peak
+                src = ("FFMA nominal 148 SM x 128 lanes x 2 x sm_max_mhz "
+                       "(no measured FP32 peak; MEASURED_PEAKS has HBM/bf16 only)")
+                name = "partial_contract_kernel (tiler + incremental FFMA contraction)"
+                bound = "fp32"
+                executed = 2 * d * kern["device_counters"]["dots"]
+            r_con = {"kernel": name, "bound": bound, "achieved": round(tf, 2),
+                     "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(tf / peak, 4),
+                     "traffic": None, "peak_source": src,
                      "alg_flops_per_launch": flops / n_iter, "avg_launch_ms": tc / n_iter,
                      "share_of_step": round(tc / (tc + tg), 3),
-                     "executed_flops": 2 * d * kern["device_counters"]["dots"]}
+                     "executed_flops": executed,
+                     "note": "achieved = algorithmic flops (2*D*compulsory union cells, "
+                             "profiles/geometry_*.json) / measured contraction time"}
         if r_con is not None and tc >= tg:
             roofline, secondary = r_con, r_gather
         else:
@@ -475,6 +490,7 @@ def main():
                              "flops_alg": geom["flops_alg_run"] if geom else None},
             "kernel_ms": {k: [round(x, 4) for x in v] for k, v in kern.items()
                           if k.endswith("_ms")} if kern else None,
+            "tensor_cores": kern.get("tensor_cores") if kern else None,
             "device_counters": kern.get("device_counters") if kern else None,
             "compare": compare or None,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,

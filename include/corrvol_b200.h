@@ -184,6 +184,24 @@ int cvb_partial_gather(const cvb_partial_desc* desc, const float* f1,
                        const int32_t* meta, float* const* cache_levels_host, float* out,
                        int32_t flags, void* stream);
 
+/* Tensor-core contraction (fast path, D <= 256): the same tiler, metadata
+ * and cache as cvb_partial_contract, with the new-cell contraction on
+ * tcgen05 (kind::f16, split-fp16 operands, 3 MMAs per K-step, fp32
+ * accumulation in TMEM).  cvb_tc_prepare splits F1 (per-tile images) and the
+ * fmap2 pyramid (hi/lo planes) once per image pair; maxbits is device
+ * workspace (2 x uint32).  Not bit-exact: use cvb_partial_contract with
+ * CVB_STRICT for reference-exact arithmetic. */
+int cvb_tc_sizes(const cvb_partial_desc* desc, int64_t* f1_split_bytes,
+                 int64_t* f2_split_bytes_per_level);
+int cvb_tc_prepare(const cvb_partial_desc* desc, const float* f1,
+                   const float* const* f2_levels_host, void* f1_split,
+                   void* const* f2_split_host, uint32_t* maxbits, void* stream);
+int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
+                            const float* const* f2_levels_host, const void* f1_split,
+                            const void* const* f2_split_host, const uint32_t* maxbits,
+                            const void* coords, int32_t* meta, float* const* cache_levels_host,
+                            unsigned long long* counters, int32_t flags, void* stream);
+
 /* ---- reference block-sparse state (sparse.py:262-309) ------------------- */
 
 /* Computation mask of one level as a bitmask: row s (source tile) has

@@ -24,157 +24,26 @@
 //     memory, and combined into (2r+1)^2 taps (canonical fp64 association
 //     in STRICT mode, _pykernels.py:99-115), written coalesced per query.
 #include "gemm.cuh"
+#include "partial.cuh"
 
 namespace cvb {
-
-constexpr int TQH = CVB_TILE_H, TQW = CVB_TILE_W, TQ = TQH * TQW;  // 64 queries
-constexpr int ST_OK = 0, ST_OVERFLOW = 1, ST_EMPTY = 2;
-
-struct PartialParams {
-  const float* f1;
-  int h1, w1, d, levels, radius;
-  const float* f2[CVB_MAX_LEVELS];
-  float* cache[CVB_MAX_LEVELS];
-  int th[CVB_MAX_LEVELS], tw[CVB_MAX_LEVELS], ch[CVB_MAX_LEVELS], cw[CVB_MAX_LEVELS];
-  const void* coords;
-  int32_t* meta;
-  unsigned long long* counters;
-  int tiles_x;
-  int64_t n_tiles;
-  float scale;
-  bool f64, normalize, no_cache, vec;
-};
-
-struct Box {
-  int ylo, yhi, xlo, xhi;
-  __device__ bool empty() const { return ylo > yhi || xlo > xhi; }
-  __device__ int h() const { return yhi - ylo + 1; }
-  __device__ int w() const { return xhi - xlo + 1; }
-  __device__ int64_t area() const { return empty() ? 0 : (int64_t)h() * w(); }
-};
-
-// idx-th cell of B \ I in a fixed order (top band, bottom band, left, right).
-// I is empty or contained in B.
-__device__ __forceinline__ void new_cell(const Box& B, const Box& I, bool has_i, int idx, int& cy,
-                                         int& cx) {
-  const int wB = B.w();
-  if (!has_i) {
-    cy = B.ylo + idx / wB;
-    cx = B.xlo + idx % wB;
-    return;
-  }
-  const int n1 = (I.ylo - B.ylo) * wB;
-  if (idx < n1) {
-    cy = B.ylo + idx / wB;
-    cx = B.xlo + idx % wB;
-    return;
-  }
-  idx -= n1;
-  const int n2 = (B.yhi - I.yhi) * wB;
-  if (idx < n2) {
-    cy = I.yhi + 1 + idx / wB;
-    cx = B.xlo + idx % wB;
-    return;
-  }
-  idx -= n2;
-  const int wl = I.xlo - B.xlo;
-  const int n3 = I.h() * wl;
-  if (idx < n3) {
-    cy = I.ylo + idx / wl;
-    cx = B.xlo + idx % wl;
-    return;
-  }
-  idx -= n3;
-  const int wr = B.xhi - I.xhi;
-  cy = I.ylo + idx / wr;
-  cx = I.xhi + 1 + idx % wr;
-}
-
-__device__ __forceinline__ int slot_of(int cy, int cx, int ch, int cw) {
-  return (cy % ch) * cw + (cx % cw);
-}
 
 template <bool STRICT>
 __global__ void __launch_bounds__(GEMM_THREADS) partial_contract_kernel(PartialParams P) {
   __shared__ __align__(16) float smem[GEMM_SMEM_FLOATS];
-  __shared__ int s_red[4];  // min_ay, max_ay, min_ax, max_ax
-  __shared__ int s_nvalid;
-  __shared__ Box s_B, s_I;
-  __shared__ int s_has_i, s_n_new;
+  __shared__ int s_red[5];
+  __shared__ TilePlan s_plan;
 
   const int64_t tile = blockIdx.x;
   const int level = blockIdx.y;
   const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
-  const int th = P.th[level], tw = P.tw[level], r = P.radius;
+  const int tw = P.tw[level];
   const int tid = threadIdx.x;
-
-  if (tid == 0) {
-    s_red[0] = INT_MAX;
-    s_red[1] = INT_MIN;
-    s_red[2] = INT_MAX;
-    s_red[3] = INT_MIN;
-    s_nvalid = 0;
-  }
-  __syncthreads();
-  if (tid < TQ) {
-    const int py = tile_y * TQH + tid / TQW, px = tile_x * TQW + tid % TQW;
-    if (py < P.h1 && px < P.w1) {
-      double x, y;
-      load_coord(P.coords, P.f64, (int64_t)py * P.w1 + px, x, y);
-      const LevelPos lp = level_pos(x, y, level);
-      const int ay = clamp_anchor(lp.y0, r, th), ax = clamp_anchor(lp.x0, r, tw);
-      atomicMin(&s_red[0], ay);
-      atomicMax(&s_red[1], ay);
-      atomicMin(&s_red[2], ax);
-      atomicMax(&s_red[3], ax);
-      atomicAdd(&s_nvalid, 1);
-    }
-  }
-  __syncthreads();
-  int32_t* meta = P.meta + (tile * P.levels + level) * CVB_META_INTS;
-  if (tid == 0) {
-    Box B;
-    B.ylo = max(s_red[0] - r, 0);
-    B.yhi = min(s_red[1] + r + 1, th - 1);
-    B.xlo = max(s_red[2] - r, 0);
-    B.xhi = min(s_red[3] + r + 1, tw - 1);
-    int status = ST_OK;
-    if (s_nvalid == 0 || B.empty()) {
-      status = ST_EMPTY;
-      B = Box{1, 0, 1, 0};
-    } else if (B.h() > P.ch[level] || B.w() > P.cw[level]) {
-      status = ST_OVERFLOW;
-    }
-    Box prev{meta[0], meta[1], meta[2], meta[3]};
-    const bool prev_ok = !P.no_cache && meta[4] == ST_OK && !prev.empty();
-    Box I{max(B.ylo, prev.ylo), min(B.yhi, prev.yhi), max(B.xlo, prev.xlo),
-          min(B.xhi, prev.xhi)};
-    const bool has_i = status == ST_OK && prev_ok && !I.empty();
-    const int n_new = status == ST_OK ? (int)(B.area() - (has_i ? I.area() : 0)) : 0;
-    s_B = B;
-    s_I = I;
-    s_has_i = has_i;
-    s_n_new = n_new;
-    meta[0] = B.ylo;
-    meta[1] = B.yhi;
-    meta[2] = B.xlo;
-    meta[3] = B.xhi;
-    meta[4] = status;
-    meta[5] = n_new;
-    if (P.counters != nullptr) {
-      if (n_new > 0) {
-        atomicAdd(P.counters + 0, (unsigned long long)n_new * s_nvalid);
-        atomicAdd(P.counters + 1, (unsigned long long)n_new);
-      }
-      if (status == ST_OVERFLOW) atomicAdd(P.counters + 2, 1ULL);
-      if (status == ST_EMPTY) atomicAdd(P.counters + 3, 1ULL);
-    }
-  }
-  __syncthreads();
-  const int n_new = s_n_new;
+  plan_tile_level(P, tile, level, &s_plan, s_red);
+  const int n_new = s_plan.n_new;
   if (n_new == 0) return;
-  const Box B = s_B, I = s_I;
-  const bool has_i = s_has_i;
+  const Box B = s_plan.B, I = s_plan.I;
+  const bool has_i = s_plan.has_i;
   const int ch = P.ch[level], cw = P.cw[level];
   const float* f2 = P.f2[level];
   float* cache = P.cache[level] + tile * (int64_t)(ch * cw) * TQ;
@@ -215,47 +84,76 @@ __global__ void __launch_bounds__(GEMM_THREADS) partial_contract_kernel(PartialP
   }
 }
 
+// K2: one warp per query row of the tile (8 queries); 4 warps per CTA, so a
+// tile is two CTAs.  The union of the 8 supports (unclipped) is staged into
+// shared memory as region[ry][rx][8 queries] with 16-byte loads of the cache
+// (each cell holds the 8 queries' costs in one 32-byte sector); cells outside
+// the grid stay zero, so every tap reads its 4 corners without bounds tests.
+// Oversized regions and overflowed tiles take a per-query fallback.
+constexpr int K2_WARPS = 4;
+constexpr int K2_REGION_CELLS = 288;  // per warp: 288 cells x 8 queries x 4 B = 9 KB
+
 template <bool STRICT>
-__global__ void __launch_bounds__(256) partial_sample_kernel(PartialParams P, float* out) {
-  extern __shared__ __align__(16) float ps_smem[];
-  const int r = P.radius, S = 2 * r + 2, K = 2 * r + 1, SS = S * S, KK = K * K;
+__device__ __forceinline__ void emit_taps(const float* __restrict__ R, int stride_cell, int rw,
+                                          int oy, int ox, int K, int t0, int tstep, double fx,
+                                          double fy, float scale, bool normalize,
+                                          float* __restrict__ o) {
+  const Weights64 w64 = weights64(fx, fy);
+  const Weights32 w32 = weights32(fx, fy);
+  int dy = t0 / K, dx = t0 % K;
+  const int row = rw * stride_cell;
+  for (int t = t0; t < K * K; t += tstep) {
+    const float* c = R + ((oy + dy) * rw + (ox + dx)) * stride_cell;
+    const float v00 = c[0], v01 = c[stride_cell], v10 = c[row], v11 = c[row + stride_cell];
+    float v = STRICT ? combine64(v00, v01, v10, v11, w64) : combine32(v00, v01, v10, v11, w32);
+    if (normalize) v = __fmul_rn(v, scale);
+    o[t] = v;
+    dx += tstep;
+    while (dx >= K) {
+      dx -= K;
+      ++dy;
+    }
+  }
+}
+
+template <bool STRICT>
+__global__ void __launch_bounds__(K2_WARPS * 32) partial_sample_kernel(PartialParams P, float* out) {
+  __shared__ __align__(16) float s_region[K2_WARPS][K2_REGION_CELLS * TQW];
+  __shared__ int s_ay[K2_WARPS][TQW], s_ax[K2_WARPS][TQW], s_valid[K2_WARPS][TQW];
+  __shared__ double s_fx[K2_WARPS][TQW], s_fy[K2_WARPS][TQW];
+
+  const int r = P.radius, S = 2 * r + 2, K = 2 * r + 1, KK = K * K;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tile = blockIdx.x;
+  const int64_t tile = blockIdx.x >> 1;
   const int level = blockIdx.y;
   const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
   const int th = P.th[level], tw = P.tw[level];
-  const int py = tile_y * TQH + warp;
+  const int qrow = (blockIdx.x & 1) * K2_WARPS + warp;  // query row inside the tile
+  const int py = tile_y * TQH + qrow;
   if (py >= P.h1) return;  // warp-uniform
 
-  // per-warp shared state: patches [8][SS], anchors, weights
-  float* patch = ps_smem + warp * (TQW * SS);
-  int* s_ay = reinterpret_cast<int*>(ps_smem + 8 * TQW * SS) + warp * (4 * TQW);
-  int* s_ax = s_ay + TQW;
-  int* s_valid = s_ax + TQW;
-  double* s_fx = reinterpret_cast<double*>(ps_smem + 8 * TQW * SS + 8 * 4 * TQW) + warp * 2 * TQW;
-  double* s_fy = s_fx + TQW;
-
-  for (int c = lane; c < TQW * SS; c += 32) patch[c] = 0.f;
   int ay = 0, ax = 0, valid = 0;
   if (lane < TQW) {
     const int px = tile_x * TQW + lane;
     valid = px < P.w1;
+    double fx = 0.0, fy = 0.0;
     if (valid) {
       double x, y;
       load_coord(P.coords, P.f64, (int64_t)py * P.w1 + px, x, y);
       const LevelPos lp = level_pos(x, y, level);
       ay = clamp_anchor(lp.y0, r, th);
       ax = clamp_anchor(lp.x0, r, tw);
-      s_fx[lane] = lp.fx;
-      s_fy[lane] = lp.fy;
+      fx = lp.fx;
+      fy = lp.fy;
     }
-    s_ay[lane] = ay;
-    s_ax[lane] = ax;
-    s_valid[lane] = valid;
+    s_ay[warp][lane] = ay;
+    s_ax[warp][lane] = ax;
+    s_valid[warp][lane] = valid;
+    s_fx[warp][lane] = fx;
+    s_fy[warp][lane] = fy;
   }
-  // warp union of supports, clipped to the grid
-  int ylo = valid ? ay - r : INT_MAX, yhi = valid ? ay + r + 1 : INT_MIN;
-  int xlo = valid ? ax - r : INT_MAX, xhi = valid ? ax + r + 1 : INT_MIN;
+  int ylo = valid ? ay : INT_MAX, yhi = valid ? ay : INT_MIN;
+  int xlo = valid ? ax : INT_MAX, xhi = valid ? ax : INT_MIN;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     ylo = min(ylo, __shfl_xor_sync(0xffffffffu, ylo, o));
@@ -264,57 +162,94 @@ __global__ void __launch_bounds__(256) partial_sample_kernel(PartialParams P, fl
     xhi = max(xhi, __shfl_xor_sync(0xffffffffu, xhi, o));
   }
   __syncwarp();
+  if (ylo > yhi) return;  // no valid query in this row
+  // unclipped union of the supports
+  ylo -= r;
+  yhi += r + 1;
+  xlo -= r;
+  xhi += r + 1;
+  const int rh = yhi - ylo + 1, rw = xhi - xlo + 1;
   const int32_t* meta = P.meta + (tile * P.levels + level) * CVB_META_INTS;
   const int status = meta[4];
-  const int q = lane & 7, sub = lane >> 3;
-  const int qay = s_ay[q], qax = s_ax[q], qvalid = s_valid[q];
-  ylo = max(ylo, 0);
-  yhi = min(yhi, th - 1);
-  xlo = max(xlo, 0);
-  xhi = min(xhi, tw - 1);
-  if (status == ST_OK && ylo <= yhi && xlo <= xhi) {
-    const int ch = P.ch[level], cw = P.cw[level];
-    const float* cache = P.cache[level] + tile * (int64_t)(ch * cw) * TQ + warp * TQW;
-    const int rw = xhi - xlo + 1;
-    const int n = (yhi - ylo + 1) * rw;
-    for (int c = sub; c < n; c += 4) {
-      const int cy = ylo + c / rw, cx = xlo + c % rw;
-      const float v = __ldg(cache + (int64_t)slot_of(cy, cx, ch, cw) * TQ + q);
-      const int j = cy - (qay - r), i = cx - (qax - r);
-      if (qvalid && j >= 0 && j < S && i >= 0 && i < S) patch[q * SS + j * S + i] = v;
-    }
-  } else if (status == ST_OVERFLOW) {
-    // direct evaluation of each query's in-grid support cells
-    const int d = P.d;
-    const float* f2 = P.f2[level];
-    for (int e = lane; e < TQW * SS; e += 32) {
-      const int qq = e / SS, c = e % SS;
-      if (!s_valid[qq]) continue;
-      const int cy = s_ay[qq] - r + c / S, cx = s_ax[qq] - r + c % S;
-      if (cy < 0 || cy >= th || cx < 0 || cx >= tw) continue;
-      const float* a = P.f1 + ((int64_t)py * P.w1 + tile_x * TQW + qq) * d;
-      const float* b = f2 + ((int64_t)cy * tw + cx) * d;
-      float acc = 0.f;
-      for (int k = 0; k < d; ++k) acc = mac<STRICT>(acc, __ldg(a + k), __ldg(b + k));
-      patch[e] = acc;
-    }
-  }
-  __syncwarp();
+  const int ch = P.ch[level], cw = P.cw[level];
+  const float* cache = P.cache[level] + tile * (int64_t)(ch * cw) * TQ + qrow * TQW;
   const int64_t row0 = (int64_t)py * P.w1 + tile_x * TQW;
-  for (int e = lane; e < TQW * KK; e += 32) {
-    const int qq = e / KK, t = e % KK;
-    if (!s_valid[qq]) continue;
-    const Weights64 w64 = weights64(s_fx[qq], s_fy[qq]);
-    const Weights32 w32 = weights32(s_fx[qq], s_fy[qq]);
-    out[((row0 + qq) * P.levels + level) * (int64_t)KK + t] = tap_from_patch<STRICT>(
-        patch + qq * SS, S, t / K, t % K, w64, w32, P.scale, P.normalize);
-  }
-}
+  float* R = s_region[warp];
 
-static size_t sample_smem_bytes(int radius) {
-  const int S = 2 * radius + 2;
-  return (size_t)8 * TQW * S * S * sizeof(float) + (size_t)8 * 4 * TQW * sizeof(int) +
-         (size_t)8 * 2 * TQW * sizeof(double);
+  if (status != ST_OVERFLOW && rh * rw <= K2_REGION_CELLS) {
+    // ---- stage the region: (cell, half) units, 8 independent 16-byte loads
+    // in flight per lane.  In-grid cells of the region lie in the tile box B
+    // (<= cap), so their slot row/col is the first in-grid cell's slot plus an
+    // offset < cap (one conditional subtraction, no modulo).
+    const int gy0 = max(ylo, 0), gx0 = max(xlo, 0);
+    const int ym = gy0 % ch, xm = gx0 % cw;
+    const bool ok = status == ST_OK;
+    const int n_units = rh * rw * 2;
+    const float inv_rw = 1.0f / (float)rw;
+    constexpr int UNR = 8;
+    for (int u0 = 0; u0 < n_units; u0 += 32 * UNR) {
+      float4 v[UNR];
+      int soff[UNR];
+#pragma unroll
+      for (int k = 0; k < UNR; ++k) {
+        const int u = u0 + k * 32 + lane;
+        const int cell = u >> 1, half = u & 1;
+        const int ry = (int)(((float)cell + 0.5f) * inv_rw);
+        const int rx = cell - ry * rw;
+        const int cy = ylo + ry, cx = xlo + rx;
+        soff[k] = u < n_units ? cell * TQW + half * 4 : -1;
+        v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (u < n_units && ok && cy >= 0 && cy < th && cx >= 0 && cx < tw) {
+          int srow = ym + (cy - gy0);
+          if (srow >= ch) srow -= ch;
+          int scol = xm + (cx - gx0);
+          if (scol >= cw) scol -= cw;
+          v[k] = __ldg(reinterpret_cast<const float4*>(cache + (int64_t)(srow * cw + scol) * TQ +
+                                                       half * 4));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < UNR; ++k)
+        if (soff[k] >= 0) *reinterpret_cast<float4*>(R + soff[k]) = v[k];
+    }
+    __syncwarp();
+    // ---- taps: 4 lanes per query ----
+    const int q = lane >> 2, sub = lane & 3;
+    if (s_valid[warp][q]) {
+      const int oy = s_ay[warp][q] - r - ylo, ox = s_ax[warp][q] - r - xlo;
+      emit_taps<STRICT>(R + q, TQW, rw, oy, ox, K, sub, 4, s_fx[warp][q], s_fy[warp][q],
+                        P.scale, P.normalize, out + ((row0 + q) * P.levels + level) * (int64_t)KK);
+    }
+    return;
+  }
+
+  // ---- fallback: one query at a time through a (2r+2)^2 patch ----
+  const int d = P.d;
+  const float* f2 = P.f2[level];
+  for (int q = 0; q < TQW; ++q) {
+    if (!s_valid[warp][q]) continue;
+    const int qay = s_ay[warp][q], qax = s_ax[warp][q];
+    for (int c = lane; c < S * S; c += 32) {
+      const int cy = qay - r + c / S, cx = qax - r + c % S;
+      float v = 0.f;
+      if (cy >= 0 && cy < th && cx >= 0 && cx < tw) {
+        if (status == ST_OK) {
+          v = __ldg(cache + (int64_t)slot_of(cy, cx, ch, cw) * TQ + q);
+        } else if (status == ST_OVERFLOW) {
+          const float* a = P.f1 + (row0 + q) * d;
+          const float* b = f2 + ((int64_t)cy * tw + cx) * d;
+          float acc = 0.f;
+          for (int k = 0; k < d; ++k) acc = mac<STRICT>(acc, __ldg(a + k), __ldg(b + k));
+          v = acc;
+        }
+      }
+      R[c] = v;
+    }
+    __syncwarp();
+    emit_taps<STRICT>(R, 1, S, 0, 0, K, lane, 32, s_fx[warp][q], s_fy[warp][q], P.scale,
+                      P.normalize, out + ((row0 + q) * P.levels + level) * (int64_t)KK);
+    __syncwarp();
+  }
 }
 
 }  // namespace cvb
@@ -361,7 +296,8 @@ int cvb_partial_reset(const cvb_partial_desc* desc, int32_t* meta, void* stream)
   return check_launch("partial_reset");
 }
 
-static int build_params(const cvb_partial_desc* desc, const float* f1,
+__attribute__((visibility("hidden"))) int cvb_internal_build_params(
+    const cvb_partial_desc* desc, const float* f1,
                         const float* const* f2_levels_host, const void* coords, float scale,
                         int32_t* meta, float* const* cache_levels_host,
                         unsigned long long* counters, int32_t flags, PartialParams& P) {
@@ -420,19 +356,11 @@ static int launch_contract(const PartialParams& P, int32_t flags, cudaStream_t s
 static int launch_gather(const PartialParams& P, float* out, int32_t flags, cudaStream_t s) {
   if (P.n_tiles == 0) return CVB_OK;
   CVB_REQUIRE(out, "partial_sample: null output");
-  dim3 grid((unsigned)P.n_tiles, (unsigned)P.levels);
-  const size_t smem = sample_smem_bytes(P.radius);
-  if (flags & CVB_STRICT) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(partial_sample_kernel<true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    partial_sample_kernel<true><<<grid, 256, smem, s>>>(P, out);
-  } else {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(partial_sample_kernel<false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    partial_sample_kernel<false><<<grid, 256, smem, s>>>(P, out);
-  }
+  dim3 grid((unsigned)(2 * P.n_tiles), (unsigned)P.levels);
+  if (flags & CVB_STRICT)
+    partial_sample_kernel<true><<<grid, K2_WARPS * 32, 0, s>>>(P, out);
+  else
+    partial_sample_kernel<false><<<grid, K2_WARPS * 32, 0, s>>>(P, out);
   return check_launch("partial_sample");
 }
 
@@ -441,7 +369,7 @@ int cvb_partial_sample(const cvb_partial_desc* desc, const float* f1,
                        int32_t* meta, float* const* cache_levels_host, float* out,
                        unsigned long long* counters, int32_t flags, void* stream) {
   PartialParams P;
-  int st = build_params(desc, f1, f2_levels_host, coords, scale, meta, cache_levels_host,
+  int st = cvb_internal_build_params(desc, f1, f2_levels_host, coords, scale, meta, cache_levels_host,
                         counters, flags, P);
   if (st != CVB_OK) return st;
   st = launch_contract(P, flags, as_stream(stream));
@@ -454,7 +382,7 @@ int cvb_partial_contract(const cvb_partial_desc* desc, const float* f1,
                          float* const* cache_levels_host, unsigned long long* counters,
                          int32_t flags, void* stream) {
   PartialParams P;
-  int st = build_params(desc, f1, f2_levels_host, coords, 1.0f, meta, cache_levels_host,
+  int st = cvb_internal_build_params(desc, f1, f2_levels_host, coords, 1.0f, meta, cache_levels_host,
                         counters, flags, P);
   if (st != CVB_OK) return st;
   return launch_contract(P, flags, as_stream(stream));
@@ -465,7 +393,7 @@ int cvb_partial_gather(const cvb_partial_desc* desc, const float* f1,
                        const int32_t* meta, float* const* cache_levels_host, float* out,
                        int32_t flags, void* stream) {
   PartialParams P;
-  int st = build_params(desc, f1, f2_levels_host, coords, scale, const_cast<int32_t*>(meta),
+  int st = cvb_internal_build_params(desc, f1, f2_levels_host, coords, scale, const_cast<int32_t*>(meta),
                         cache_levels_host, nullptr, flags, P);
   if (st != CVB_OK) return st;
   return launch_gather(P, out, flags, as_stream(stream));

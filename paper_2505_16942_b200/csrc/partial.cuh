@@ -1,0 +1,167 @@
+// Shared definitions of the partial sampler's tile path (csrc/partial.cu,
+// csrc/partial_tc.cu): query tiles, the window-union tiler and the toroidal
+// tile-cache addressing.  See partial.cu for the design.
+#pragma once
+#include "common.cuh"
+
+namespace cvb {
+
+constexpr int TQH = CVB_TILE_H, TQW = CVB_TILE_W, TQ = TQH * TQW;  // 64 queries
+constexpr int ST_OK = 0, ST_OVERFLOW = 1, ST_EMPTY = 2;
+
+struct PartialParams {
+  const float* f1;
+  int h1, w1, d, levels, radius;
+  const float* f2[CVB_MAX_LEVELS];
+  float* cache[CVB_MAX_LEVELS];
+  int th[CVB_MAX_LEVELS], tw[CVB_MAX_LEVELS], ch[CVB_MAX_LEVELS], cw[CVB_MAX_LEVELS];
+  const void* coords;
+  int32_t* meta;
+  unsigned long long* counters;
+  int tiles_x;
+  int64_t n_tiles;
+  float scale;
+  bool f64, normalize, no_cache, vec;
+};
+
+struct Box {
+  int ylo, yhi, xlo, xhi;
+  __device__ bool empty() const { return ylo > yhi || xlo > xhi; }
+  __device__ int h() const { return yhi - ylo + 1; }
+  __device__ int w() const { return xhi - xlo + 1; }
+  __device__ int64_t area() const { return empty() ? 0 : (int64_t)h() * w(); }
+};
+
+// idx-th cell of B \ I in a fixed order (top band, bottom band, left, right).
+// I is empty or contained in B.
+__device__ __forceinline__ void new_cell(const Box& B, const Box& I, bool has_i, int idx, int& cy,
+                                         int& cx) {
+  const int wB = B.w();
+  if (!has_i) {
+    cy = B.ylo + idx / wB;
+    cx = B.xlo + idx % wB;
+    return;
+  }
+  const int n1 = (I.ylo - B.ylo) * wB;
+  if (idx < n1) {
+    cy = B.ylo + idx / wB;
+    cx = B.xlo + idx % wB;
+    return;
+  }
+  idx -= n1;
+  const int n2 = (B.yhi - I.yhi) * wB;
+  if (idx < n2) {
+    cy = I.yhi + 1 + idx / wB;
+    cx = B.xlo + idx % wB;
+    return;
+  }
+  idx -= n2;
+  const int wl = I.xlo - B.xlo;
+  const int n3 = I.h() * wl;
+  if (idx < n3) {
+    cy = I.ylo + idx / wl;
+    cx = B.xlo + idx % wl;
+    return;
+  }
+  idx -= n3;
+  const int wr = B.xhi - I.xhi;
+  cy = I.ylo + idx / wr;
+  cx = I.xhi + 1 + idx % wr;
+}
+
+__device__ __forceinline__ int slot_of(int cy, int cx, int ch, int cw) {
+  return (cy % ch) * cw + (cx % cw);
+}
+
+// Result of the window-union tiler for one (tile, level).
+struct TilePlan {
+  Box B, I;
+  int has_i, n_new, nvalid, status;
+};
+
+// Window-union tiler for one (tile, level); every thread of the CTA must call
+// it (blockDim >= 64).  Bounding box of the tile's (2r+2)^2 supports (offsets
+// -r..r+1 around floor(x/2^l), sparse.py:279) clipped to the level grid;
+// compares with the previous box in `meta`, decides OK / OVERFLOW / EMPTY,
+// writes the new meta and counters.  `plan` and `red` are shared memory.
+__device__ __forceinline__ void plan_tile_level(const PartialParams& P, int64_t tile, int level,
+                                                TilePlan* plan, int* red) {
+  const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
+  const int th = P.th[level], tw = P.tw[level], r = P.radius;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    red[0] = INT_MAX;
+    red[1] = INT_MIN;
+    red[2] = INT_MAX;
+    red[3] = INT_MIN;
+    red[4] = 0;
+  }
+  __syncthreads();
+  if (tid < TQ) {
+    const int py = tile_y * TQH + tid / TQW, px = tile_x * TQW + tid % TQW;
+    if (py < P.h1 && px < P.w1) {
+      double x, y;
+      load_coord(P.coords, P.f64, (int64_t)py * P.w1 + px, x, y);
+      const LevelPos lp = level_pos(x, y, level);
+      const int ay = clamp_anchor(lp.y0, r, th), ax = clamp_anchor(lp.x0, r, tw);
+      atomicMin(&red[0], ay);
+      atomicMax(&red[1], ay);
+      atomicMin(&red[2], ax);
+      atomicMax(&red[3], ax);
+      atomicAdd(&red[4], 1);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int32_t* meta = P.meta + (tile * P.levels + level) * CVB_META_INTS;
+    const int nvalid = red[4];
+    Box B;
+    B.ylo = max(red[0] - r, 0);
+    B.yhi = min(red[1] + r + 1, th - 1);
+    B.xlo = max(red[2] - r, 0);
+    B.xhi = min(red[3] + r + 1, tw - 1);
+    int status = ST_OK;
+    if (nvalid == 0 || B.empty()) {
+      status = ST_EMPTY;
+      B = Box{1, 0, 1, 0};
+    } else if (B.h() > P.ch[level] || B.w() > P.cw[level]) {
+      status = ST_OVERFLOW;
+    }
+    const Box prev{meta[0], meta[1], meta[2], meta[3]};
+    const bool prev_ok = !P.no_cache && meta[4] == ST_OK && !prev.empty();
+    const Box I{max(B.ylo, prev.ylo), min(B.yhi, prev.yhi), max(B.xlo, prev.xlo),
+                min(B.xhi, prev.xhi)};
+    const bool has_i = status == ST_OK && prev_ok && !I.empty();
+    const int n_new = status == ST_OK ? (int)(B.area() - (has_i ? I.area() : 0)) : 0;
+    plan->B = B;
+    plan->I = I;
+    plan->has_i = has_i;
+    plan->n_new = n_new;
+    plan->nvalid = nvalid;
+    plan->status = status;
+    meta[0] = B.ylo;
+    meta[1] = B.yhi;
+    meta[2] = B.xlo;
+    meta[3] = B.xhi;
+    meta[4] = status;
+    meta[5] = n_new;
+    if (P.counters != nullptr) {
+      if (n_new > 0) {
+        atomicAdd(P.counters + 0, (unsigned long long)n_new * nvalid);
+        atomicAdd(P.counters + 1, (unsigned long long)n_new);
+      }
+      if (status == ST_OVERFLOW) atomicAdd(P.counters + 2, 1ULL);
+      if (status == ST_EMPTY) atomicAdd(P.counters + 3, 1ULL);
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace cvb
+
+extern "C" int cvb_internal_build_params(const cvb_partial_desc* desc, const float* f1,
+                                         const float* const* f2_levels_host, const void* coords,
+                                         float scale, int32_t* meta,
+                                         float* const* cache_levels_host,
+                                         unsigned long long* counters, int32_t flags,
+                                         cvb::PartialParams& P);

@@ -252,6 +252,10 @@ class SparseVolumeState:
         self.desc: Optional[_lib.PartialDesc] = None
         self.meta: Optional[torch.Tensor] = None
         self._src_tile = None
+        self.tc = False
+        self.tc_f1 = None
+        self.tc_f2 = None
+        self.tc_max = None
 
     # -- reference-compatible attributes ------------------------------------
     @property
@@ -307,13 +311,16 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
                cache_cap_bytes: Optional[int] = None, hard_limit_bytes: Optional[int] = None,
                growth_factor: int = 2, cache_enabled: bool = True,
                backend: Optional[str] = None, mode: str = "tile", strict: bool = False,
-               tile_caps=None, pyramid: Optional[FeaturePyramid] = None) -> SparseVolumeState:
+               tile_caps=None, pyramid: Optional[FeaturePyramid] = None,
+               tensor_cores: Optional[bool] = None) -> SparseVolumeState:
     """One-time preprocessing for an image pair (sparse.py:205-248).
 
     Builds the fmap2 pyramid on the GPU and allocates the level states.
     mode="tile": cache window per level from tile_caps (default
     DEFAULT_TILE_CAPS); hard_limit_bytes bounds the preallocated tile cache.
     mode="block": reference block store per level (growth, cap, hard limit).
+    tensor_cores (tile mode, fast arithmetic): contract on tcgen05 with
+    split-fp16 operands (default when not strict and D <= 256).
     """
     resolve_backend(backend)
     if f1.dims != f2.dims:
@@ -361,6 +368,12 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
             lv.cache = torch.empty(per_level[lvl], dtype=torch.float32, device=dev)
         _lib.call("cvb_partial_reset", _lib.C.byref(desc), _lib.ptr(state.meta),
                   stream_handle())
+        if tensor_cores is None:
+            tensor_cores = (not strict) and f1.dims <= 256
+        if tensor_cores:
+            if strict:
+                raise ValueError("strict arithmetic runs on the FP32 pipe; tensor_cores=False")
+            _prepare_tc(state)
     else:
         for lv in levels:
             n_src, wpr = pm1.n_tiles, lv.words_per_row
@@ -371,6 +384,51 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
                                   overalloc_cap_bytes=cache_cap_bytes,
                                   hard_limit_bytes=hard_limit_bytes, device=dev)
     return state
+
+
+def _prepare_tc(state: SparseVolumeState) -> None:
+    """Split F1 / the fmap2 pyramid into fp16 hi/lo operands (once per pair)."""
+    spec = state.spec
+    f1b = _lib.C.c_int64()
+    per = (_lib.C.c_int64 * _lib.MAX_LEVELS)()
+    _lib.call("cvb_tc_sizes", _lib.C.byref(state.desc), _lib.C.byref(f1b), per)
+    dev = state.device
+    state.tc_f1 = torch.empty(f1b.value, dtype=torch.uint8, device=dev)
+    state.tc_f2 = [torch.empty(per[l], dtype=torch.uint8, device=dev)
+                   for l in range(spec.levels)]
+    state.tc_max = torch.zeros(2, dtype=torch.int32, device=dev)
+    f2s = [state.pyramid.levels[l].values for l in range(spec.levels)]
+    _lib.call("cvb_tc_prepare", _lib.C.byref(state.desc), _lib.ptr(state.f1.values),
+              _lib.ptr_array(f2s), _lib.ptr(state.tc_f1), _lib.ptr_array(state.tc_f2),
+              _lib.ptr(state.tc_max), stream_handle())
+    state.tc = True
+
+
+def _contract_args(state: SparseVolumeState, centroids: CentroidField, flags: int):
+    spec = state.spec
+    f2s = _lib.ptr_array([state.pyramid.levels[l].values for l in range(spec.levels)])
+    caches = _lib.ptr_array([lv.cache for lv in state.levels])
+    return f2s, caches
+
+
+def _contract(state: SparseVolumeState, centroids: CentroidField, flags: int, f2s,
+              caches) -> None:
+    if state.tc:
+        _lib.call("cvb_partial_contract_tc", _lib.C.byref(state.desc), _lib.ptr(state.f1.values),
+                  f2s, _lib.ptr(state.tc_f1), _lib.ptr_array(state.tc_f2),
+                  _lib.ptr(state.tc_max), _lib.ptr(centroids.coords), _lib.ptr(state.meta),
+                  caches, _lib.ptr(state._dev_counters), flags, stream_handle())
+    else:
+        _lib.call("cvb_partial_contract", _lib.C.byref(state.desc), _lib.ptr(state.f1.values),
+                  f2s, _lib.ptr(centroids.coords), _lib.ptr(state.meta), caches,
+                  _lib.ptr(state._dev_counters), flags, stream_handle())
+
+
+def _gather(state: SparseVolumeState, centroids: CentroidField, flags: int, f2s, caches,
+            out: torch.Tensor) -> None:
+    _lib.call("cvb_partial_gather", _lib.C.byref(state.desc), _lib.ptr(state.f1.values), f2s,
+              _lib.ptr(centroids.coords), state.spec.scale(state.f1.dims), _lib.ptr(state.meta),
+              caches, _lib.ptr(out), flags, stream_handle())
 
 
 def _level_centroid_floors(state: SparseVolumeState, centroids: CentroidField, level: int):
@@ -539,16 +597,12 @@ def _sample_block_mode(state: SparseVolumeState, centroids: CentroidField,
 
 def _sample_tile_mode(state: SparseVolumeState, centroids: CentroidField,
                       out: torch.Tensor) -> None:
-    spec = state.spec
     flags = coords_flags(centroids, state.strict)
     if not state.cache_enabled:
         flags |= _lib.CVB_NO_CACHE
-    f2s = [state.pyramid.levels[l].values for l in range(spec.levels)]
-    caches = [lv.cache for lv in state.levels]
-    _lib.call("cvb_partial_sample", _lib.C.byref(state.desc), _lib.ptr(state.f1.values),
-              _lib.ptr_array(f2s), _lib.ptr(centroids.coords), spec.scale(state.f1.dims),
-              _lib.ptr(state.meta), _lib.ptr_array(caches), _lib.ptr(out),
-              _lib.ptr(state._dev_counters), flags, stream_handle())
+    f2s, caches = _contract_args(state, centroids, flags)
+    _contract(state, centroids, flags, f2s, caches)
+    _gather(state, centroids, flags, f2s, caches, out)
 
 
 def sample_iteration(state: SparseVolumeState, centroids: CentroidField,
@@ -619,22 +673,15 @@ def sample_iteration_timed(state: SparseVolumeState, centroids: CentroidField,
     if state.mode != "tile":
         raise ValueError("timed iterations need a tile-mode state")
     _check_grid(state, centroids)
-    spec = state.spec
     flags = coords_flags(centroids, state.strict)
     if not state.cache_enabled:
         flags |= _lib.CVB_NO_CACHE
-    f2s = _lib.ptr_array([state.pyramid.levels[l].values for l in range(spec.levels)])
-    caches = _lib.ptr_array([lv.cache for lv in state.levels])
+    f2s, caches = _contract_args(state, centroids, flags)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    s = stream_handle()
     ev[0].record()
-    _lib.call("cvb_partial_contract", _lib.C.byref(state.desc), _lib.ptr(state.f1.values), f2s,
-              _lib.ptr(centroids.coords), _lib.ptr(state.meta), caches,
-              _lib.ptr(state._dev_counters), flags, s)
+    _contract(state, centroids, flags, f2s, caches)
     ev[1].record()
-    _lib.call("cvb_partial_gather", _lib.C.byref(state.desc), _lib.ptr(state.f1.values), f2s,
-              _lib.ptr(centroids.coords), spec.scale(state.f1.dims), _lib.ptr(state.meta),
-              caches, _lib.ptr(out), flags, s)
+    _gather(state, centroids, flags, f2s, caches, out)
     ev[2].record()
     state.iteration += 1
     return tuple(ev)
