@@ -212,8 +212,10 @@ class Clocks:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for row in rows:
             try:
-                sm.append(float(row[1]))
                 smax = float(row[2])
+                if float(row[1]) < 0.3 * smax:  # idle sample (before the first launch)
+                    continue
+                sm.append(float(row[1]))
                 for nm, v in zip(names, row[5:9]):
                     if v.strip().lower() == "active":
                         reasons.add(nm)
@@ -305,12 +307,15 @@ def main():
         return
 
     # ---- main measurement: inputs resident in HBM -------------------------
+    # nvidia-smi samples clocks from before the warm-up to the end of the timed
+    # region (the GPU is under load the whole time); it needs ~1 s to start.
+    clocks = Clocks(local).start()
+    time.sleep(1.5)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     torch.cuda.reset_peak_memory_stats(dev)
     base_alloc = torch.cuda.memory_allocated(dev)
-    clocks = Clocks(local).start()
     launches0 = _lib.launch_count()
     ms_step = timed(step, args.steps, 0)
     launches = _lib.launch_count() - launches0

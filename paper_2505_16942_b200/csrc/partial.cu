@@ -79,7 +79,9 @@ __global__ void __launch_bounds__(GEMM_THREADS) partial_contract_kernel(PartialP
       int cy, cx;
       new_cell(B, I, has_i, idx, cy, cx);
       float4 v = make_float4(acc[0][j], acc[1][j], acc[2][j], acc[3][j]);
-      *reinterpret_cast<float4*>(cache + (int64_t)slot_of(cy, cx, ch, cw) * TQ + ty * 4) = v;
+      // cache layout [query row][slot][8 queries]; queries ty*4..ty*4+3
+      *reinterpret_cast<float4*>(
+          cache + ((int64_t)(ty >> 1) * (ch * cw) + slot_of(cy, cx, ch, cw)) * TQW + (ty & 1) * 4) = v;
     }
   }
 }
@@ -91,7 +93,8 @@ __global__ void __launch_bounds__(GEMM_THREADS) partial_contract_kernel(PartialP
 // the grid stay zero, so every tap reads its 4 corners without bounds tests.
 // Oversized regions and overflowed tiles take a per-query fallback.
 constexpr int K2_WARPS = 4;
-constexpr int K2_REGION_CELLS = 288;  // per warp: 288 cells x 8 queries x 4 B = 9 KB
+constexpr int K2_REGION_CELLS = 256;  // per warp: 256 cells x 8 queries x 4 B = 8 KB
+constexpr int K2_MAX_TAPS = 81;       // staged outputs per query (r <= 4); larger r: fallback
 
 template <bool STRICT>
 __device__ __forceinline__ void emit_taps(const float* __restrict__ R, int stride_cell, int rw,
@@ -121,6 +124,10 @@ __global__ void __launch_bounds__(K2_WARPS * 32) partial_sample_kernel(PartialPa
   __shared__ __align__(16) float s_region[K2_WARPS][K2_REGION_CELLS * TQW];
   __shared__ int s_ay[K2_WARPS][TQW], s_ax[K2_WARPS][TQW], s_valid[K2_WARPS][TQW];
   __shared__ double s_fx[K2_WARPS][TQW], s_fy[K2_WARPS][TQW];
+  __shared__ Weights64 s_w64[K2_WARPS][TQW];
+  __shared__ Weights32 s_w32[K2_WARPS][TQW];
+  __shared__ __align__(16) float s_out[K2_WARPS][TQW * K2_MAX_TAPS];
+  __shared__ __align__(8) uint64_t s_bar[K2_WARPS];
 
   const int r = P.radius, S = 2 * r + 2, K = 2 * r + 1, KK = K * K;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -131,6 +138,12 @@ __global__ void __launch_bounds__(K2_WARPS * 32) partial_sample_kernel(PartialPa
   const int qrow = (blockIdx.x & 1) * K2_WARPS + warp;  // query row inside the tile
   const int py = tile_y * TQH + qrow;
   if (py >= P.h1) return;  // warp-uniform
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_bar[warp]))
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
 
   int ay = 0, ax = 0, valid = 0;
   if (lane < TQW) {
@@ -151,95 +164,168 @@ __global__ void __launch_bounds__(K2_WARPS * 32) partial_sample_kernel(PartialPa
     s_valid[warp][lane] = valid;
     s_fx[warp][lane] = fx;
     s_fy[warp][lane] = fy;
-  }
-  int ylo = valid ? ay : INT_MAX, yhi = valid ? ay : INT_MIN;
-  int xlo = valid ? ax : INT_MAX, xhi = valid ? ax : INT_MIN;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    ylo = min(ylo, __shfl_xor_sync(0xffffffffu, ylo, o));
-    yhi = max(yhi, __shfl_xor_sync(0xffffffffu, yhi, o));
-    xlo = min(xlo, __shfl_xor_sync(0xffffffffu, xlo, o));
-    xhi = max(xhi, __shfl_xor_sync(0xffffffffu, xhi, o));
+    s_w64[warp][lane] = weights64(fx, fy);
+    s_w32[warp][lane] = weights32(fx, fy);
   }
   __syncwarp();
-  if (ylo > yhi) return;  // no valid query in this row
-  // unclipped union of the supports
-  ylo -= r;
-  yhi += r + 1;
-  xlo -= r;
-  xhi += r + 1;
-  const int rh = yhi - ylo + 1, rw = xhi - xlo + 1;
   const int32_t* meta = P.meta + (tile * P.levels + level) * CVB_META_INTS;
   const int status = meta[4];
   const int ch = P.ch[level], cw = P.cw[level];
-  const float* cache = P.cache[level] + tile * (int64_t)(ch * cw) * TQ + qrow * TQW;
+  // this warp's plane of the tile cache: [slot][8 queries]
+  const float* cache = P.cache[level] + (tile * TQH + qrow) * (int64_t)(ch * cw) * TQW;
   const int64_t row0 = (int64_t)py * P.w1 + tile_x * TQW;
   float* R = s_region[warp];
+  float* O = s_out[warp];
+  const uint32_t rbase = (uint32_t)__cvta_generic_to_shared(R);
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar[warp]);
+  const unsigned valid_mask = __ballot_sync(0xffffffffu, valid) & 0xFFu;
+  unsigned done = ~valid_mask & 0xFFu;  // invalid queries need nothing
+  uint32_t phase = 0;
 
-  if (status != ST_OVERFLOW && rh * rw <= K2_REGION_CELLS) {
-    // ---- stage the region: (cell, half) units, 8 independent 16-byte loads
-    // in flight per lane.  In-grid cells of the region lie in the tile box B
-    // (<= cap), so their slot row/col is the first in-grid cell's slot plus an
-    // offset < cap (one conditional subtraction, no modulo).
-    const int gy0 = max(ylo, 0), gx0 = max(xlo, 0);
-    const int ym = gy0 % ch, xm = gx0 % cw;
-    const bool ok = status == ST_OK;
-    const int n_units = rh * rw * 2;
-    const float inv_rw = 1.0f / (float)rw;
-    constexpr int UNR = 8;
-    for (int u0 = 0; u0 < n_units; u0 += 32 * UNR) {
-      float4 v[UNR];
-      int soff[UNR];
+  // Fast path over query groups: all 8 queries share one staged region; if
+  // their union does not fit, two groups of 4 (divergent flow), then the
+  // per-query fallback below.
+  if (status != ST_OVERFLOW && KK <= K2_MAX_TAPS) {
+    for (int gsz = TQW; gsz >= 4 && done != 0xFFu; gsz >>= 1) {
+      for (int g0 = 0; g0 < TQW; g0 += gsz) {
+        const unsigned gmask = ((1u << gsz) - 1u) << g0;
+        const unsigned todo = gmask & ~done;
+        if (todo == 0) continue;
+        const bool mine = lane < TQW && ((todo >> lane) & 1u);
+        int ylo = mine ? ay : INT_MAX, yhi = mine ? ay : INT_MIN;
+        int xlo = mine ? ax : INT_MAX, xhi = mine ? ax : INT_MIN;
 #pragma unroll
-      for (int k = 0; k < UNR; ++k) {
-        const int u = u0 + k * 32 + lane;
-        const int cell = u >> 1, half = u & 1;
-        const int ry = (int)(((float)cell + 0.5f) * inv_rw);
-        const int rx = cell - ry * rw;
-        const int cy = ylo + ry, cx = xlo + rx;
-        soff[k] = u < n_units ? cell * TQW + half * 4 : -1;
-        v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (u < n_units && ok && cy >= 0 && cy < th && cx >= 0 && cx < tw) {
-          int srow = ym + (cy - gy0);
-          if (srow >= ch) srow -= ch;
-          int scol = xm + (cx - gx0);
-          if (scol >= cw) scol -= cw;
-          v[k] = __ldg(reinterpret_cast<const float4*>(cache + (int64_t)(srow * cw + scol) * TQ +
-                                                       half * 4));
+        for (int o = 16; o > 0; o >>= 1) {
+          ylo = min(ylo, __shfl_xor_sync(0xffffffffu, ylo, o));
+          yhi = max(yhi, __shfl_xor_sync(0xffffffffu, yhi, o));
+          xlo = min(xlo, __shfl_xor_sync(0xffffffffu, xlo, o));
+          xhi = max(xhi, __shfl_xor_sync(0xffffffffu, xhi, o));
         }
+        // unclipped union of the group's supports
+        ylo -= r;
+        yhi += r + 1;
+        xlo -= r;
+        xhi += r + 1;
+        const int rh = yhi - ylo + 1, rw = xhi - xlo + 1;
+        if (rh * rw > K2_REGION_CELLS) continue;  // try smaller groups
+        // ---- stage the region: each in-grid region row is one contiguous run
+        // of slots in this warp's cache plane (two if it wraps the toroidal
+        // column), fetched with one bulk async copy per run; cells outside the
+        // grid are zero-filled first.  In-grid cells of the region lie in the
+        // tile box B (<= cap): slot = first in-grid slot + offset < cap.
+        const bool ok = status == ST_OK;
+        const int gy0 = max(ylo, 0), gy1 = min(yhi, th - 1);
+        const int gx0 = max(xlo, 0), gx1 = min(xhi, tw - 1);
+        const bool any = ok && gy0 <= gy1 && gx0 <= gx1;
+        const bool full = any && gy0 == ylo && gy1 == yhi && gx0 == xlo && gx1 == xhi;
+        if (!full) {
+          float4* z = reinterpret_cast<float4*>(R);
+          for (int i = lane; i < rh * rw * 2; i += 32) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (any) {
+          const int nrow = gy1 - gy0 + 1, ncol = gx1 - gx0 + 1;
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                         "r"((uint32_t)(nrow * ncol * TQW * 4))
+                         : "memory");
+          __syncwarp();
+          const int ym = gy0 % ch, xm = gx0 % cw;
+          const int n1 = min(ncol, cw - xm);  // cells before the column wrap
+          for (int i = lane; i < nrow; i += 32) {
+            int srow = ym + i;
+            if (srow >= ch) srow -= ch;
+            const float* src = cache + (int64_t)(srow * cw + xm) * TQW;
+            const uint32_t dst =
+                rbase + (uint32_t)(((gy0 - ylo + i) * rw + (gx0 - xlo)) * TQW * 4);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+                "%2, [%3];" ::"r"(dst),
+                "l"(src), "r"((uint32_t)(n1 * TQW * 4)), "r"(bar)
+                : "memory");
+            if (ncol > n1)
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+                  "%2, [%3];" ::"r"(dst + (uint32_t)(n1 * TQW * 4)),
+                  "l"(cache + (int64_t)(srow * cw) * TQW), "r"((uint32_t)((ncol - n1) * TQW * 4)),
+                  "r"(bar)
+                  : "memory");
+          }
+          asm volatile(
+              "{\n\t.reg .pred P1;\n"
+              "LAB_WAIT:\n\t"
+              "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+              "@P1 bra.uni DONE;\n\t"
+              "bra.uni LAB_WAIT;\n"
+              "DONE:\n\t}\n" ::"r"(bar),
+              "r"(phase)
+              : "memory");
+          phase ^= 1u;
+        }
+        // ---- taps: one (query, tap row) per lane-iteration; the two region
+        // rows a tap row needs are read once (K+1 cells each) and combined in
+        // registers; results staged in shared memory for coalesced stores.
+        for (int e = lane; e < TQW * K; e += 32) {
+          const int q = e & (TQW - 1), dy = e >> 3;
+          if (!((todo >> q) & 1u)) continue;
+          const float* a =
+              R + ((s_ay[warp][q] - r - ylo + dy) * rw + (s_ax[warp][q] - r - xlo)) * TQW + q;
+          const float* b = a + rw * TQW;
+          const Weights32 w32 = s_w32[warp][q];
+          const Weights64 w64 = s_w64[warp][q];
+          float* o = O + q * KK + dy * K;
+          float a0 = a[0], b0 = b[0];
+          for (int i = 0; i < K; ++i) {
+            const float a1 = a[(i + 1) * TQW], b1 = b[(i + 1) * TQW];
+            float v = STRICT ? combine64(a0, a1, b0, b1, w64) : combine32(a0, a1, b0, b1, w32);
+            if (P.normalize) v = __fmul_rn(v, P.scale);
+            o[i] = v;
+            a0 = a1;
+            b0 = b1;
+          }
+        }
+        __syncwarp();
+        for (int q = g0; q < g0 + gsz; ++q) {
+          if (!((todo >> q) & 1u)) continue;
+          float* dst = out + ((row0 + q) * P.levels + level) * (int64_t)KK;
+          for (int t = lane; t < KK; t += 32) dst[t] = O[q * KK + t];
+        }
+        __syncwarp();
+        done |= todo;
       }
-#pragma unroll
-      for (int k = 0; k < UNR; ++k)
-        if (soff[k] >= 0) *reinterpret_cast<float4*>(R + soff[k]) = v[k];
     }
-    __syncwarp();
-    // ---- taps: 4 lanes per query ----
-    const int q = lane >> 2, sub = lane & 3;
-    if (s_valid[warp][q]) {
-      const int oy = s_ay[warp][q] - r - ylo, ox = s_ax[warp][q] - r - xlo;
-      emit_taps<STRICT>(R + q, TQW, rw, oy, ox, K, sub, 4, s_fx[warp][q], s_fy[warp][q],
-                        P.scale, P.normalize, out + ((row0 + q) * P.levels + level) * (int64_t)KK);
-    }
-    return;
   }
+  if (done == 0xFFu) return;
 
   // ---- fallback: one query at a time through a (2r+2)^2 patch ----
   const int d = P.d;
   const float* f2 = P.f2[level];
   for (int q = 0; q < TQW; ++q) {
-    if (!s_valid[warp][q]) continue;
+    if ((done >> q) & 1u) continue;
     const int qay = s_ay[warp][q], qax = s_ax[warp][q];
+    const float* a = P.f1 + (row0 + q) * d;
     for (int c = lane; c < S * S; c += 32) {
       const int cy = qay - r + c / S, cx = qax - r + c % S;
       float v = 0.f;
       if (cy >= 0 && cy < th && cx >= 0 && cx < tw) {
         if (status == ST_OK) {
-          v = __ldg(cache + (int64_t)slot_of(cy, cx, ch, cw) * TQ + q);
+          v = __ldg(cache + (int64_t)slot_of(cy, cx, ch, cw) * TQW + q);
         } else if (status == ST_OVERFLOW) {
-          const float* a = P.f1 + (row0 + q) * d;
           const float* b = f2 + ((int64_t)cy * tw + cx) * d;
           float acc = 0.f;
-          for (int k = 0; k < d; ++k) acc = mac<STRICT>(acc, __ldg(a + k), __ldg(b + k));
+          if (P.vec) {
+            for (int k = 0; k < d; k += 4) {
+              const float4 x = __ldg(reinterpret_cast<const float4*>(a + k));
+              const float4 y = __ldg(reinterpret_cast<const float4*>(b + k));
+              acc = mac<STRICT>(acc, x.x, y.x);
+              acc = mac<STRICT>(acc, x.y, y.y);
+              acc = mac<STRICT>(acc, x.z, y.z);
+              acc = mac<STRICT>(acc, x.w, y.w);
+            }
+          } else {
+            for (int k = 0; k < d; ++k) acc = mac<STRICT>(acc, __ldg(a + k), __ldg(b + k));
+          }
           v = acc;
         }
       }

@@ -251,7 +251,8 @@ __global__ void __launch_bounds__(THREADS) partial_contract_tc_kernel(TcParams T
   __shared__ __align__(8) uint64_t bars[NST + 2];  // stage_free[NST], acc_full, b_full
   __shared__ uint32_t s_tmem;
   __shared__ TilePlan s_plan[CVB_MAX_LEVELS];
-  __shared__ int s_red[5];
+  __shared__ int s_red[CVB_MAX_LEVELS][2][4];
+  __shared__ int s_nvalid;
   __shared__ int s_prefix[CVB_MAX_LEVELS + 1];
 
   const PartialParams& P = T.P;
@@ -273,6 +274,7 @@ __global__ void __launch_bounds__(THREADS) partial_contract_tc_kernel(TcParams T
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (tid == 32) {
+    s_nvalid = 0;
     for (int i = 0; i < NST + 2; ++i) mbar_init(bar_stage + 8 * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -291,7 +293,7 @@ __global__ void __launch_bounds__(THREADS) partial_contract_tc_kernel(TcParams T
   }
 
   // window-union tiler for every level (overlaps the B copy)
-  for (int l = 0; l < P.levels; ++l) plan_tile_level(P, tile, l, &s_plan[l], s_red);
+  plan_tile_all_levels(P, tile, s_plan, s_red, &s_nvalid);
   if (tid == 0) {
     s_prefix[0] = 0;
     for (int l = 0; l < P.levels; ++l) s_prefix[l + 1] = s_prefix[l] + s_plan[l].n_new;
@@ -308,8 +310,7 @@ __global__ void __launch_bounds__(THREADS) partial_contract_tc_kernel(TcParams T
   const __half* src_hi = nullptr;
   const __half* src_lo = nullptr;
 
-  auto issue_loads = [&](int step) {
-    const int c = step / n_ks, ks = step % n_ks, st = step % NST;
+  auto issue_loads = [&](int c, int ks, int st) {
     if (c != load_chunk) {
       load_chunk = c;
       src_hi = nullptr;
@@ -331,23 +332,37 @@ __global__ void __launch_bounds__(THREADS) partial_contract_tc_kernel(TcParams T
     cp_async_commit();
   };
 
-  if (n_steps > 0) issue_loads(0);
+  if (n_steps > 0) issue_loads(0, 0, 0);
   if (tid == 0) mbar_wait(bar_b, 0);
   const float s_main = ldexpf(1.f, -(scale_exp(T.maxbits[0]) + scale_exp(T.maxbits[1])));
   const float s_corr = s_main * (1.f / (float)(1 << LOG2_LO));
 
+  // step i = (chunk c, k-slice ks) uses stage st = i % NST; its n-th use
+  // (n = i / NST) completes phase n of stage_free[st]
+  int c = 0, ks = 0, st = 0;
+  int nc = 0, nks = 1, nst = 1 % NST, nuse = (1 >= NST) ? 1 : 0;  // next step, stage use count
+  if (nks == n_ks) {
+    nks = 0;
+    ++nc;
+  }
   for (int i = 0; i < n_steps; ++i) {
     if (i + 1 < n_steps) {
-      const int nxt = i + 1;
-      if (nxt >= NST) mbar_wait(bar_stage + 8 * (nxt % NST), ((nxt / NST) - 1) & 1);
-      issue_loads(nxt);
+      if (i + 1 >= NST) mbar_wait(bar_stage + 8 * nst, (nuse - 1) & 1);
+      issue_loads(nc, nks, nst);
       cp_async_wait<1>();
+      if (++nks == n_ks) {
+        nks = 0;
+        ++nc;
+      }
+      if (++nst == NST) {
+        nst = 0;
+        ++nuse;
+      }
     } else {
       cp_async_wait<0>();
     }
     fence_proxy_async();
     __syncthreads();
-    const int c = i / n_ks, ks = i % n_ks, st = i % NST;
     if (tid == 0) {
       tc_fence_after();
       const uint32_t a_hi = sA + st * A_STAGE, a_lo = a_hi + A_HALF;
@@ -373,11 +388,14 @@ __global__ void __launch_bounds__(THREADS) partial_contract_tc_kernel(TcParams T
       const int g = c * M + tid;
       const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
       float vm[32], vc[32];
-      float* dst = nullptr;
+      float* dst = nullptr;  // tile block of the cell's level: [query row][slot][8]
+      int64_t plane = 0, slot = 0;
       if (g < n_cells) {
         const CellRef cr = cell_of(g, s_plan, s_prefix, P.levels);
         const int ch = P.ch[cr.level], cw = P.cw[cr.level];
-        dst = P.cache[cr.level] + (tile * (int64_t)(ch * cw) + slot_of(cr.cy, cr.cx, ch, cw)) * TQ;
+        plane = (int64_t)ch * cw * TQW;
+        slot = slot_of(cr.cy, cr.cx, ch, cw);
+        dst = P.cache[cr.level] + tile * plane * TQH + slot * TQW;
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -391,13 +409,19 @@ __global__ void __launch_bounds__(THREADS) partial_contract_tc_kernel(TcParams T
             o.y = fmaf(vc[j + 1], s_corr, vm[j + 1] * s_main);
             o.z = fmaf(vc[j + 2], s_corr, vm[j + 2] * s_main);
             o.w = fmaf(vc[j + 3], s_corr, vm[j + 3] * s_main);
-            *reinterpret_cast<float4*>(dst + h * 32 + j) = o;
+            const int q = h * 32 + j;  // queries q..q+3 share query row q/8
+            *reinterpret_cast<float4*>(dst + (q >> 3) * plane + (q & 7)) = o;
           }
         }
       }
       tc_fence_before();
       __syncthreads();
     }
+    if (++ks == n_ks) {
+      ks = 0;
+      ++c;
+    }
+    if (++st == NST) st = 0;
   }
   if (n_steps == 0 && tid == 0) mbar_wait(bar_b, 0);
   tc_fence_before();

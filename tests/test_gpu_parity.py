@@ -293,3 +293,31 @@ def test_float32_coords_match_float64_reference(cuda):
         assert c32.coords.dtype == torch.float32
         want = O.lookup(sc.f1, sc.f2, coords.astype(np.float64), 4, 2, True)
         assert np.array_equal(cvb.sample_iteration(st, c32).numpy(), want)
+
+
+@pytest.mark.parametrize("spread", [6.0, 14.0])
+def test_divergent_flow_group_split_and_overflow(cuda, spread):
+    """Random per-pixel displacements: query rows whose supports do not fit one
+    staged region (group split / per-query fallback) and tile boxes larger than
+    the cache window (overflow path) must still be bit-exact (strict) and
+    within tolerance (fast)."""
+    rng = np.random.default_rng(int(spread))
+    h, w, d = 33, 47, 24
+    spec = cvb.LookupSpec(4, 3)
+    f1n = rng.standard_normal((h, w, d)).astype(np.float32)
+    f2n = rng.standard_normal((h, w, d)).astype(np.float32)
+    f1 = cvb.FeatureMap(torch.from_numpy(f1n).to(cuda))
+    f2 = cvb.FeatureMap(torch.from_numpy(f2n).to(cuda))
+    strict = cvb.init_state(f1, f2, spec, strict=True)
+    fast = cvb.init_state(f1, f2, spec)
+    ys, xs = np.mgrid[0:h, 0:w]
+    base = np.stack([xs, ys], -1).astype(np.float64)
+    for it in range(3):
+        coords = base + rng.uniform(-spread, spread, size=base.shape)
+        want = O.lookup(f1n, f2n, coords, 4, 3)
+        c = cvb.CentroidField(torch.from_numpy(coords).to(cuda))
+        assert np.array_equal(cvb.sample_iteration(strict, c).numpy(), want)
+        got = cvb.sample_iteration(fast, c).numpy()
+        assert O.deviation(got, want, want) <= REF_GATE
+    if spread > 10:
+        assert strict.device_counters["overflow_tile_levels"] > 0
