@@ -116,10 +116,14 @@ def reference_sample(cfg: str, workers: int, rows_per_worker: int):
     if _REF_SC is None:
         _REF_SC = (cv, _RefScenario(cfg))
     sc = _REF_SC[1]
-    start = (sc.h // 2) // 8 * 8
-    bands = [(start + i * rows_per_worker, start + (i + 1) * rows_per_worker)
-             for i in range(workers)]
-    bands = [(a % sc.h // 8 * 8, min(a % sc.h // 8 * 8 + rows_per_worker, sc.h)) for a, _ in bands]
+    # disjoint bands spread over the frame, starting at multiples of 8 rows
+    n_slots = max(1, sc.h // rows_per_worker)
+    workers = min(workers, n_slots)
+    picks = sorted({int(round(i * (n_slots - 1) / max(1, workers - 1))) for i in range(workers)})
+    if workers == 1:
+        picks = [n_slots // 2]
+    bands = [(p * rows_per_worker, min((p + 1) * rows_per_worker, sc.h)) for p in picks]
+    workers = len(bands)
     t0 = time.perf_counter()
     if workers == 1:
         res = [_ref_band_job(bands[0])]
@@ -130,7 +134,7 @@ def reference_sample(cfg: str, workers: int, rows_per_worker: int):
     wall = time.perf_counter() - t0
     prep = statistics.mean(r[0] for r in res)
     iters = statistics.mean(r[1] for r in res)
-    rows_done = rows_per_worker * workers
+    rows_done = sum(b - a for a, b in bands)
     frame_s = prep + iters * sc.h / rows_done
     return {"ms_per_iter": 1e3 * frame_s / sc.iters, "frame_s": frame_s, "wall_s": wall,
             "prep_s": prep, "iters_s_per_band": iters, "bands": bands, "cores": workers,
@@ -146,11 +150,14 @@ def run_reference_arm(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cores = len(os.sched_getaffinity(0))
+    # one process per core on disjoint 8-row bands; capped at 16 processes so
+    # the per-process fmap2 pyramid + patch-major copies fit in host memory
+    cores = min(len(os.sched_getaffinity(0)), 16)
     h, w, d, r, levels, n_iter, norm = CONFIGS[args.config]
     times = []
     for i in range(args.warmup + args.steps):
         res = reference_sample(args.config, cores, 8)
+        cores = res["cores"]
         if i >= args.warmup:
             times.append(res["ms_per_iter"])
     v = statistics.mean(times)

@@ -151,6 +151,11 @@ typedef struct {
   int32_t tw[CVB_MAX_LEVELS];
   int32_t cap_h[CVB_MAX_LEVELS];        /* toroidal cache window per level */
   int32_t cap_w[CVB_MAX_LEVELS];
+  /* tile range [tile_begin, tile_end) processed by contract/gather/sample
+   * (row-major 8x8 tiles; tile_end <= tile_begin means all tiles).  Disjoint
+   * ranges may run concurrently; gather(range) depends only on
+   * contract(range) of the same iteration. */
+  int32_t tile_begin, tile_end;
 } cvb_partial_desc;
 
 /* tiles = ceil(h1/8)*ceil(w1/8); meta is int32 [tiles, levels, 8]; cache for

@@ -47,6 +47,7 @@ class PartialDesc(C.Structure):
         ("levels", _i32), ("radius", _i32),
         ("th", _i32 * MAX_LEVELS), ("tw", _i32 * MAX_LEVELS),
         ("cap_h", _i32 * MAX_LEVELS), ("cap_w", _i32 * MAX_LEVELS),
+        ("tile_begin", _i32), ("tile_end", _i32),
     ]
 
 

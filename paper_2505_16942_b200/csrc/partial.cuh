@@ -19,7 +19,8 @@ struct PartialParams {
   int32_t* meta;
   unsigned long long* counters;
   int tiles_x;
-  int64_t n_tiles;
+  int64_t n_tiles;       // all tiles of the frame
+  int64_t tile0, ntile;  // range handled by this launch
   float scale;
   bool f64, normalize, no_cache, vec;
 };
@@ -245,6 +246,9 @@ __device__ __forceinline__ void plan_tile_all_levels(const PartialParams& P, int
   }
   __syncthreads();
 }
+
+// gather/sampler launch (csrc/gather.cu)
+int launch_gather_kernel(const PartialParams& P, float* out, bool strict, cudaStream_t s);
 
 }  // namespace cvb
 

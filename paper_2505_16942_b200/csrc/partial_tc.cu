@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(THREADS) partial_contract_tc_kernel(TcParams T
 
   const PartialParams& P = T.P;
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int64_t tile = blockIdx.x;
+  const int64_t tile = P.tile0 + blockIdx.x;
   const int dp = T.dp;
   const uint32_t half_bytes = (uint32_t)N * dp * 2;  // one of hi / lo
   const uint32_t b_bytes = 2 * half_bytes;
@@ -507,7 +507,7 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
     T.plane[l] = used ? (int64_t)desc->th[l] * desc->tw[l] * T.dp : 0;
     if (used) CVB_REQUIRE(T.f2s[l], "partial_contract_tc: null level pointer");
   }
-  if (T.P.n_tiles == 0) return CVB_OK;
+  if (T.P.ntile == 0) return CVB_OK;
   const size_t smem = (size_t)2 * tc::N * T.dp * 2 + (size_t)tc::NST * tc::A_STAGE;
   static bool attr_set = false;
   if (!attr_set) {
@@ -515,7 +515,7 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(tc::MAX_DP * 2 * 2 * tc::N + tc::NST * tc::A_STAGE));
     attr_set = true;
   }
-  tc::partial_contract_tc_kernel<<<(unsigned)T.P.n_tiles, tc::THREADS, smem, as_stream(stream)>>>(T);
+  tc::partial_contract_tc_kernel<<<(unsigned)T.P.ntile, tc::THREADS, smem, as_stream(stream)>>>(T);
   return check_launch("partial_contract_tc");
 }
 

@@ -253,6 +253,10 @@ class SparseVolumeState:
         self.meta: Optional[torch.Tensor] = None
         self._src_tile = None
         self.tc = False
+        self.pipeline_splits = 1
+        self._side_stream = None
+        self._desc_cache = {}
+        self.n_tiles = 0
         self.tc_f1 = None
         self.tc_f2 = None
         self.tc_max = None
@@ -312,7 +316,8 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
                growth_factor: int = 2, cache_enabled: bool = True,
                backend: Optional[str] = None, mode: str = "tile", strict: bool = False,
                tile_caps=None, pyramid: Optional[FeaturePyramid] = None,
-               tensor_cores: Optional[bool] = None) -> SparseVolumeState:
+               tensor_cores: Optional[bool] = None,
+               pipeline_splits: Optional[int] = None) -> SparseVolumeState:
     """One-time preprocessing for an image pair (sparse.py:205-248).
 
     Builds the fmap2 pyramid on the GPU and allocates the level states.
@@ -363,6 +368,7 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
             raise CacheLimitError(
                 f"tile cache needs {total} bytes, hard limit is {hard_limit_bytes}")
         state.desc = desc
+        state.n_tiles = n_tiles.value
         state.meta = torch.empty(meta_ints.value, dtype=torch.int32, device=dev)
         for lvl, lv in enumerate(levels):
             lv.cache = torch.empty(per_level[lvl], dtype=torch.float32, device=dev)
@@ -374,6 +380,13 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
             if strict:
                 raise ValueError("strict arithmetic runs on the FP32 pipe; tensor_cores=False")
             _prepare_tc(state)
+            # overlap contraction and gathering across tile ranges when the frame
+            # spans many waves (>= 8 tiles per SM)
+            if pipeline_splits is None:
+                # measured on B200 at C4: no gain (the contraction's shared
+                # memory keeps the sampler from co-residing), so off by default
+                pipeline_splits = 1
+            state.pipeline_splits = max(1, int(pipeline_splits))
     else:
         for lv in levels:
             n_src, wpr = pm1.n_tiles, lv.words_per_row
@@ -595,14 +608,60 @@ def _sample_block_mode(state: SparseVolumeState, centroids: CentroidField,
         raise GatherMissError("a proxy gather hit a block that was never computed")
 
 
+def _range_descs(state: SparseVolumeState, splits: int):
+    """PartialDesc copies covering `splits` contiguous tile ranges."""
+    key = ("ranges", splits)
+    if state._desc_cache.get(key) is None:
+        n = state.n_tiles
+        bounds = [n * i // splits for i in range(splits + 1)]
+        descs = []
+        for i in range(splits):
+            d = _lib.PartialDesc()
+            _lib.C.pointer(d)[0] = state.desc
+            d.tile_begin, d.tile_end = bounds[i], bounds[i + 1]
+            descs.append(d)
+        state._desc_cache[key] = descs
+    return state._desc_cache[key]
+
+
 def _sample_tile_mode(state: SparseVolumeState, centroids: CentroidField,
                       out: torch.Tensor) -> None:
+    """Contract then gather.  On the tensor-core path the frame is cut into
+    tile ranges and gather(range i) runs on a side stream while contract(range
+    i+1) runs on the caller's stream: the memory-bound sampler overlaps the
+    latency-bound contraction.  gather(range) depends only on contract(range)
+    of the same iteration; the caller's stream joins the side stream at the
+    end, so the next iteration's contraction never races this one's gather."""
     flags = coords_flags(centroids, state.strict)
     if not state.cache_enabled:
         flags |= _lib.CVB_NO_CACHE
     f2s, caches = _contract_args(state, centroids, flags)
-    _contract(state, centroids, flags, f2s, caches)
-    _gather(state, centroids, flags, f2s, caches, out)
+    splits = state.pipeline_splits
+    if splits <= 1:
+        _contract(state, centroids, flags, f2s, caches)
+        _gather(state, centroids, flags, f2s, caches, out)
+        return
+    main = torch.cuda.current_stream(state.device)
+    if state._side_stream is None:
+        state._side_stream = torch.cuda.Stream(state.device)
+    side = state._side_stream
+    out.record_stream(side)
+    centroids.coords.record_stream(side)
+    full = state.desc
+    try:
+        for d in _range_descs(state, splits):
+            state.desc = d
+            _contract(state, centroids, flags, f2s, caches)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            side.wait_event(ev)
+            with torch.cuda.stream(side):
+                _gather(state, centroids, flags, f2s, caches, out)
+    finally:
+        state.desc = full
+    ev = torch.cuda.Event()
+    ev.record(side)
+    main.wait_event(ev)
 
 
 def sample_iteration(state: SparseVolumeState, centroids: CentroidField,

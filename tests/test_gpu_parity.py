@@ -321,3 +321,21 @@ def test_divergent_flow_group_split_and_overflow(cuda, spread):
         assert O.deviation(got, want, want) <= REF_GATE
     if spread > 10:
         assert strict.device_counters["overflow_tile_levels"] > 0
+
+
+def test_pipelined_tile_ranges_equal_single_launch(cuda):
+    """Contract/gather over tile ranges on two streams == one launch, bit for bit."""
+    spec = cvb.LookupSpec(4, 4)
+    sc = cvb.gen_scenario(4, (70, 90, 64), 4, spec, coords_dtype=np.float32)
+    f1 = cvb.FeatureMap(torch.from_numpy(sc.f1).to(cuda))
+    f2 = cvb.FeatureMap(torch.from_numpy(sc.f2).to(cuda))
+    one = cvb.init_state(f1, f2, spec, pipeline_splits=1)
+    many = cvb.init_state(f1, f2, spec, pipeline_splits=5)
+    assert one.tc and many.pipeline_splits == 5
+    for coords in sc.centroid_fields:
+        c = cvb.CentroidField(torch.from_numpy(coords).to(cuda))
+        a = cvb.sample_iteration(one, c).numpy()
+        b = cvb.sample_iteration(many, c).numpy()
+        assert np.array_equal(a, b)
+        want = O.lookup(sc.f1, sc.f2, coords, 4, 4)
+        assert O.deviation(b, want, want) <= REF_GATE
