@@ -66,7 +66,8 @@ __device__ __forceinline__ LevelPos level_pos(double x, double y, int level) {
     x = -1.0e12;
     y = -1.0e12;
   }
-  const double s = ldexp(1.0, -level);
+  // exact 2^-level from the exponent field (level < 1023)
+  const double s = __longlong_as_double((long long)(1023 - level) << 52);
   const double xl = __dmul_rn(x, s), yl = __dmul_rn(y, s);
   const double flx = floor(xl), fly = floor(yl);
   r.x0 = (long long)flx;

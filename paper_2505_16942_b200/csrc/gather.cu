@@ -32,7 +32,8 @@ constexpr int MAX_TAPS = 81;     // r <= 4 for the staged-output path
 struct QInfo {
   int ay, ax;
   double fx, fy;
-  Weights32 w32;
+  Weights32 w32;   // fp32 weights (fallback path applies the scale separately)
+  Weights32 w32s;  // fp32 weights pre-multiplied by the 1/sqrt(D) scale (fast path)
 };
 
 struct Shared {
@@ -131,12 +132,44 @@ __device__ __forceinline__ bool stage_region(float* R, uint32_t bar, const float
   return true;
 }
 
+// Fast-arithmetic taps for r=4 (K=9): lane (q, g) computes tap rows 3g..3g+2
+// of query q from 4 region rows held in registers (40 shared loads, 27 taps).
+__device__ __forceinline__ void region_taps_r4(const float* __restrict__ R, const QInfo* qi,
+                                               unsigned todo, int ylo, int xlo, int rw,
+                                               float* __restrict__ O, int lane) {
+  constexpr int K = 9, KK = 81, r = 4;
+  if (lane >= 24) return;
+  const int q = lane & 7, g = lane >> 3;
+  if (!((todo >> q) & 1u)) return;
+  const float* a = R + ((qi[q].ay - r - ylo + 3 * g) * rw + (qi[q].ax - r - xlo)) * TQW + q;
+  const Weights32 w = qi[q].w32s;
+  float* o = O + q * KK + 3 * g * K;
+  float r0[K + 1], r1[K + 1];
+#pragma unroll
+  for (int i = 0; i <= K; ++i) r0[i] = a[i * TQW];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const float* b = a + (j + 1) * rw * TQW;
+#pragma unroll
+    for (int i = 0; i <= K; ++i) r1[i] = b[i * TQW];
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+      o[j * K + i] = combine32(r0[i], r0[i + 1], r1[i], r1[i + 1], w);
+#pragma unroll
+    for (int i = 0; i <= K; ++i) r0[i] = r1[i];
+  }
+}
+
 // Taps of the queries in `todo` from a staged region into outs[q][K*K].
 template <bool STRICT, int K_>
 __device__ __forceinline__ void region_taps(const float* __restrict__ R, const QInfo* qi,
                                             unsigned todo, int ylo, int xlo, int rw, int r, int K,
                                             float scale, bool normalize, float* __restrict__ O,
                                             int lane) {
+  if (!STRICT && K_ == 9) {
+    region_taps_r4(R, qi, todo, ylo, xlo, rw, O, lane);
+    return;
+  }
   const int KK = K * K;
   for (int e = lane; e < TQW * K; e += 32) {
     const int q = e & (TQW - 1), dy = e >> 3;
@@ -171,9 +204,18 @@ __device__ __forceinline__ void region_taps(const float* __restrict__ R, const Q
   }
 }
 
+template <int KK_>
 __device__ __forceinline__ void write_outs(const float* O, unsigned todo, float* out,
                                            int64_t row0, int levels, int level, int KK,
                                            int lane) {
+  if (KK_ > 0 && todo == 0xFFu) {  // flat loop over the 8 queries' outputs
+    float* base = out + (row0 * levels + level) * (int64_t)KK_;
+    for (int e = lane; e < TQW * KK_; e += 32) {
+      const int q = e / KK_, t = e - q * KK_;
+      base[(int64_t)q * levels * KK_ + t] = O[e];
+    }
+    return;
+  }
   for (int q = 0; q < TQW; ++q) {
     if (!((todo >> q) & 1u)) continue;
     float* dst = out + ((row0 + q) * levels + level) * (int64_t)KK;
@@ -200,6 +242,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   const int r = RADIUS >= 0 ? RADIUS : P.radius;
   const int K = 2 * r + 1, KK = K * K, S = 2 * r + 2;
   constexpr int K_ = RADIUS >= 0 ? 2 * RADIUS + 1 : -1;
+  constexpr int KK_ = K_ > 0 ? K_ * K_ : -1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tile = P.tile0 + (blockIdx.x >> 1);
   const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
@@ -223,7 +266,7 @@ __global__ void __launch_bounds__(WARPS * 32)
     if (valid) load_coord(P.coords, P.f64, (int64_t)py * P.w1 + px, x, y);
     for (int li = 0; li < nlev; ++li) {
       const int l = level0 + li;
-      QInfo qi{0, 0, 0.0, 0.0, Weights32{0.f, 0.f, 0.f, 0.f}};
+      QInfo qi{0, 0, 0.0, 0.0, Weights32{0.f, 0.f, 0.f, 0.f}, Weights32{0.f, 0.f, 0.f, 0.f}};
       if (valid) {
         const LevelPos lp = level_pos(x, y, l);
         qi.ay = clamp_anchor(lp.y0, r, P.th[l]);
@@ -231,6 +274,8 @@ __global__ void __launch_bounds__(WARPS * 32)
         qi.fx = lp.fx;
         qi.fy = lp.fy;
         qi.w32 = weights32(lp.fx, lp.fy);
+        const float sc = P.normalize ? P.scale : 1.0f;
+        qi.w32s = Weights32{qi.w32.w00 * sc, qi.w32.w01 * sc, qi.w32.w10 * sc, qi.w32.w11 * sc};
       }
       sm.q[warp][li][lane] = qi;
     }
@@ -295,7 +340,7 @@ __global__ void __launch_bounds__(WARPS * 32)
         }
         region_taps<STRICT, K_>(R, qi, todo, ylo, xlo, rw, r, K, P.scale, P.normalize, O, lane);
         __syncwarp();
-        write_outs(O, todo, out, row0, P.levels, l, KK, lane);
+        write_outs<KK_>(O, todo, out, row0, P.levels, l, KK, lane);
         __syncwarp();
         done |= todo;
       }
@@ -355,7 +400,7 @@ __global__ void __launch_bounds__(WARPS * 32)
       region_taps<STRICT, K_>(sm.region[warp][b], sm.q[warp][li], vmask, g.ylo, g.xlo, g.rw, r,
                               K, P.scale, P.normalize, O, lane);
       __syncwarp();
-      write_outs(O, vmask, out, row0, P.levels, level0 + li, KK, lane);
+      write_outs<KK_>(O, vmask, out, row0, P.levels, level0 + li, KK, lane);
       __syncwarp();
     } else {
       slow_level(li, b);
