@@ -24,6 +24,7 @@
 //     removes the power-of-two scales and writes each cell's 64 query costs
 //     (256 contiguous bytes) into its cache slot.
 #include <cuda_fp16.h>
+#include <stdlib.h>
 
 #include "partial.cuh"
 
@@ -433,6 +434,411 @@ __global__ void __launch_bounds__(THREADS) partial_contract_tc_kernel(TcParams T
 }
 
 }  // namespace tc
+
+// ---------------------------------------------------------------------------
+// Persistent, warp-specialised variant (default).  One CTA per SM walks the
+// tiles blockIdx.x, blockIdx.x + gridDim.x, ...; the roles communicate only
+// through mbarrier rings, so the next tile's planning, B image and A rows are
+// in flight while the current tile's MMAs run and the previous chunk's
+// accumulators drain:
+//   warp 0       B producer: one 64 KB bulk copy per tile into a 2-deep ring
+//   warp 1       MMA issuer (one thread): 3 tcgen05.mma per K=16 step
+//   warps 2-3    planner: the window-union tiler for every level of a tile
+//   warps 4-7    A producers: one A row (cell) per thread, cp.async into a
+//                4-stage ring, fence.proxy.async + arrive once a stage landed
+//   warps 8-11   epilogue: tcgen05.ld of a 2-deep TMEM accumulator ring,
+//                main + 2^-11 corr, cache-slot stores
+// ---------------------------------------------------------------------------
+namespace tcp {
+
+constexpr int NST = 4;   // A stages
+constexpr int NB = 2;    // B buffers
+constexpr int NPL = 4;   // plan slots (the planner runs up to 3 tiles ahead)
+constexpr int THREADS = 384;
+constexpr uint32_t SPIN_LIMIT = 1u << 24;  // watchdog: trap instead of hanging
+
+struct PlanSlot {
+  TilePlan plan[CVB_MAX_LEVELS];
+  int prefix[CVB_MAX_LEVELS + 1];
+  int n_cells;
+};
+
+struct Ctl {
+  uint64_t plan_full[NPL], plan_empty[NPL];
+  uint64_t b_full[NB], b_empty[NB];
+  uint64_t a_full[NST], a_empty[NST];
+  uint64_t acc_full[2], acc_empty[2];
+  PlanSlot slot[NPL];
+  int red[CVB_MAX_LEVELS][2][4];
+  int nv[2];
+  uint32_t tmem;
+};
+
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// full barriers: the k-th completion has parity k&1; empty barriers: the
+// producer's k-th wait passes on parity (k&1)^1 (a fresh barrier counts as
+// having completed the phase before phase 0).
+__device__ __forceinline__ void wait_full(uint32_t bar, uint32_t k) {
+  for (uint32_t n = 0; !mbar_try(bar, k & 1u); ++n)
+    if (n > SPIN_LIMIT) __trap();
+}
+__device__ __forceinline__ void wait_empty(uint32_t bar, uint32_t k) {
+  for (uint32_t n = 0; !mbar_try(bar, (k & 1u) ^ 1u); ++n)
+    if (n > SPIN_LIMIT) __trap();
+}
+__device__ __forceinline__ void arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1) partial_contract_tcp_kernel(tc::TcParams T) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const PartialParams& P = T.P;
+  const int dp = T.dp;
+  const uint32_t half_bytes = (uint32_t)tc::N * dp * 2;
+  const uint32_t b_bytes = 2 * half_bytes;
+  uint8_t* sB = smem;                                   // NB x b_bytes
+  uint8_t* sA = smem + NB * b_bytes;                    // NST x A_STAGE
+  Ctl& C = *reinterpret_cast<Ctl*>(sA + NST * tc::A_STAGE);
+  const uint32_t uB = tc::smem_u32(sB), uA = tc::smem_u32(sA);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_ks = dp / tc::KS;
+  auto U = [](const uint64_t& b) { return tc::smem_u32(&b); };
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                     tc::smem_u32(&C.tmem))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 32) {
+    for (int i = 0; i < NPL; ++i) {
+      tc::mbar_init(U(C.plan_full[i]), 64);
+      tc::mbar_init(U(C.plan_empty[i]), 1 + 1 + 128 + 128);
+    }
+    for (int i = 0; i < NB; ++i) {
+      tc::mbar_init(U(C.b_full[i]), 1);
+      tc::mbar_init(U(C.b_empty[i]), 1);
+    }
+    for (int i = 0; i < NST; ++i) {
+      tc::mbar_init(U(C.a_full[i]), 128);
+      tc::mbar_init(U(C.a_empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(U(C.acc_full[i]), 1);
+      tc::mbar_init(U(C.acc_empty[i]), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = C.tmem;
+
+  if (warp == 0) {
+    // ---------------- B producer ----------------
+    if (lane == 0) {
+      uint32_t kb = 0;
+      for (int64_t it = 0;; ++it) {
+        const int64_t t = blockIdx.x + it * gridDim.x;
+        if (t >= P.ntile) break;
+        const int s = (int)(it % NPL);
+        wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
+        if (C.slot[s].n_cells > 0) {
+          const int tb = kb % NB;
+          wait_empty(U(C.b_empty[tb]), kb / NB);
+          tc::mbar_expect_tx(U(C.b_full[tb]), b_bytes);
+          const uint8_t* src = T.f1s + (P.tile0 + t) * (int64_t)b_bytes;
+          const uint32_t piece = b_bytes / 4;
+          for (int i = 0; i < 4; ++i)
+            tc::bulk_g2s(uB + tb * b_bytes + i * piece, src + i * piece, piece, U(C.b_full[tb]));
+          ++kb;
+        }
+        arrive(U(C.plan_empty[s]));
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      uint32_t kb = 0, g = 0, cg = 0;
+      for (int64_t it = 0;; ++it) {
+        const int64_t t = blockIdx.x + it * gridDim.x;
+        if (t >= P.ntile) break;
+        const int s = (int)(it % NPL);
+        wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
+        const int n = C.slot[s].n_cells;
+        if (n > 0) {
+          const int tb = kb % NB;
+          wait_full(U(C.b_full[tb]), kb / NB);
+          const uint32_t bh = uB + tb * b_bytes, bl = bh + half_bytes;
+          const int n_chunks = (n + tc::M - 1) / tc::M;
+          for (int c = 0; c < n_chunks; ++c, ++cg) {
+            const int ab = cg & 1;
+            wait_empty(U(C.acc_empty[ab]), cg >> 1);
+            tc::tc_fence_after();
+            const uint32_t d_main = tmem + ab * 128, d_corr = d_main + 64;
+            for (int ks = 0; ks < n_ks; ++ks, ++g) {
+              const int st = g % NST;
+              wait_full(U(C.a_full[st]), g / NST);
+              tc::tc_fence_after();
+              const uint32_t a_hi = uA + st * tc::A_STAGE, a_lo = a_hi + tc::A_HALF;
+#pragma unroll
+              for (int k2 = 0; k2 < tc::KS / 16; ++k2) {
+                const uint32_t kstep = ks * (tc::KS / 16) + k2;
+                const uint64_t dah = tc::make_desc(a_hi + k2 * 256, 128, (tc::KS / 8) * 128);
+                const uint64_t dal = tc::make_desc(a_lo + k2 * 256, 128, (tc::KS / 8) * 128);
+                const uint64_t dbh = tc::make_desc(bh + kstep * 256, 128, (dp / 8) * 128);
+                const uint64_t dbl = tc::make_desc(bl + kstep * 256, 128, (dp / 8) * 128);
+                const uint32_t acc = (ks > 0 || k2 > 0) ? 1u : 0u;
+                tc::mma_f16(d_main, dah, dbh, acc);
+                tc::mma_f16(d_corr, dah, dbl, acc);
+                tc::mma_f16(d_corr, dal, dbh, 1u);
+              }
+              tc::mma_commit(U(C.a_empty[st]));
+            }
+            tc::mma_commit(U(C.acc_full[ab]));
+          }
+          tc::mma_commit(U(C.b_empty[tb]));
+          ++kb;
+        }
+        arrive(U(C.plan_empty[s]));
+      }
+    }
+  } else if (warp < 4) {
+    // ---------------- planner (64 threads) ----------------
+    const int pt = tid - 64, pw = pt >> 5;
+    const int r = P.radius;
+    for (int64_t it = 0;; ++it) {
+      const int64_t t = blockIdx.x + it * gridDim.x;
+      if (t >= P.ntile) break;
+      const int64_t tile = P.tile0 + t;
+      const int s = (int)(it % NPL);
+      wait_empty(U(C.plan_empty[s]), (uint32_t)(it / NPL));
+      const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
+      const int py = tile_y * TQH + pt / TQW, px = tile_x * TQW + pt % TQW;
+      const bool valid = py < P.h1 && px < P.w1;
+      double x = 0.0, y = 0.0;
+      if (valid) load_coord(P.coords, P.f64, (int64_t)py * P.w1 + px, x, y);
+      const unsigned vote = __ballot_sync(0xffffffffu, valid);
+      if (lane == 0) C.nv[pw] = __popc(vote);
+      for (int l = 0; l < P.levels; ++l) {
+        int ylo = INT_MAX, yhi = INT_MIN, xlo = INT_MAX, xhi = INT_MIN;
+        if (valid) {
+          const LevelPos lp = level_pos(x, y, l);
+          ylo = yhi = clamp_anchor(lp.y0, r, P.th[l]);
+          xlo = xhi = clamp_anchor(lp.x0, r, P.tw[l]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          ylo = min(ylo, __shfl_xor_sync(0xffffffffu, ylo, o));
+          yhi = max(yhi, __shfl_xor_sync(0xffffffffu, yhi, o));
+          xlo = min(xlo, __shfl_xor_sync(0xffffffffu, xlo, o));
+          xhi = max(xhi, __shfl_xor_sync(0xffffffffu, xhi, o));
+        }
+        if (lane == 0) {
+          C.red[l][pw][0] = ylo;
+          C.red[l][pw][1] = yhi;
+          C.red[l][pw][2] = xlo;
+          C.red[l][pw][3] = xhi;
+        }
+      }
+      named_sync(1, 64);
+      PlanSlot& S = C.slot[s];
+      if (pt < P.levels) {
+        const int level = pt;
+        const int th = P.th[level], tw = P.tw[level];
+        int32_t* meta = P.meta + (tile * P.levels + level) * CVB_META_INTS;
+        const int nv = C.nv[0] + C.nv[1];
+        Box B;
+        B.ylo = max(min(C.red[level][0][0], C.red[level][1][0]) - r, 0);
+        B.yhi = min(max(C.red[level][0][1], C.red[level][1][1]) + r + 1, th - 1);
+        B.xlo = max(min(C.red[level][0][2], C.red[level][1][2]) - r, 0);
+        B.xhi = min(max(C.red[level][0][3], C.red[level][1][3]) + r + 1, tw - 1);
+        int status = ST_OK;
+        if (nv == 0 || B.empty()) {
+          status = ST_EMPTY;
+          B = Box{1, 0, 1, 0};
+        } else if (B.h() > P.ch[level] || B.w() > P.cw[level]) {
+          status = ST_OVERFLOW;
+        }
+        const Box prev{meta[0], meta[1], meta[2], meta[3]};
+        const bool prev_ok = !P.no_cache && meta[4] == ST_OK && !prev.empty();
+        const Box I{max(B.ylo, prev.ylo), min(B.yhi, prev.yhi), max(B.xlo, prev.xlo),
+                    min(B.xhi, prev.xhi)};
+        const bool has_i = status == ST_OK && prev_ok && !I.empty();
+        const int n_new = status == ST_OK ? (int)(B.area() - (has_i ? I.area() : 0)) : 0;
+        S.plan[level] = TilePlan{B, I, (int)has_i, n_new, nv, status};
+        meta[0] = B.ylo;
+        meta[1] = B.yhi;
+        meta[2] = B.xlo;
+        meta[3] = B.xhi;
+        meta[4] = status;
+        meta[5] = n_new;
+        if (P.counters != nullptr) {
+          if (n_new > 0) {
+            atomicAdd(P.counters + 0, (unsigned long long)n_new * nv);
+            atomicAdd(P.counters + 1, (unsigned long long)n_new);
+          }
+          if (status == ST_OVERFLOW) atomicAdd(P.counters + 2, 1ULL);
+          if (status == ST_EMPTY) atomicAdd(P.counters + 3, 1ULL);
+        }
+      }
+      named_sync(1, 64);
+      if (pt == 0) {
+        S.prefix[0] = 0;
+        for (int l = 0; l < P.levels; ++l) S.prefix[l + 1] = S.prefix[l] + S.plan[l].n_new;
+        S.n_cells = S.prefix[P.levels];
+      }
+      named_sync(1, 64);
+      arrive(U(C.plan_full[s]));
+    }
+  } else if (warp < 8) {
+    // ---------------- A producers (128 threads, one A row each) ----------------
+    const int ap = tid - 128;
+    const uint32_t row_off = (ap >> 3) * (tc::KS / 8) * 128 + (ap & 7) * 16;
+    uint32_t g = 0;
+    for (int64_t it = 0;; ++it) {
+      const int64_t t = blockIdx.x + it * gridDim.x;
+      if (t >= P.ntile) break;
+      const int s = (int)(it % NPL);
+      wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
+      const PlanSlot& S = C.slot[s];
+      const int n = S.n_cells;
+      const int n_chunks = (n + tc::M - 1) / tc::M;
+      // stages issued but not yet published (at most NST-1 in flight)
+      int n_pend = 0;
+      uint32_t pend_st0 = 0, pend_st1 = 0;
+      for (int c = 0; c < n_chunks; ++c) {
+        const __half* src_hi = nullptr;
+        const __half* src_lo = nullptr;
+        const int gi = c * tc::M + ap;
+        if (gi < n) {
+          const tc::CellRef cr = tc::cell_of(gi, S.plan, S.prefix, P.levels);
+          src_hi = T.f2s[cr.level] + ((int64_t)cr.cy * P.tw[cr.level] + cr.cx) * dp;
+          src_lo = src_hi + T.plane[cr.level];
+        }
+        for (int ks = 0; ks < n_ks; ++ks, ++g) {
+          const int st = g % NST;
+          wait_empty(U(C.a_empty[st]), g / NST);
+          if (src_hi != nullptr) {
+            const uint32_t dst = uA + st * tc::A_STAGE + row_off;
+#pragma unroll
+            for (int j = 0; j < tc::KS / 8; ++j) {
+              tc::cp_async16(dst + j * 128, src_hi + ks * tc::KS + j * 8);
+              tc::cp_async16(dst + tc::A_HALF + j * 128, src_lo + ks * tc::KS + j * 8);
+            }
+          }
+          tc::cp_async_commit();
+          if (n_pend == 2) {  // the oldest stage landed: publish it to the tensor core
+            tc::cp_async_wait<2>();
+            tc::fence_proxy_async();
+            arrive(U(C.a_full[pend_st0]));
+            pend_st0 = pend_st1;
+            pend_st1 = st;
+          } else if (n_pend == 1) {
+            pend_st1 = st;
+            n_pend = 2;
+          } else {
+            pend_st0 = st;
+            n_pend = 1;
+          }
+        }
+      }
+      if (n_pend == 2) {
+        tc::cp_async_wait<1>();
+        tc::fence_proxy_async();
+        arrive(U(C.a_full[pend_st0]));
+        pend_st0 = pend_st1;
+        n_pend = 1;
+      }
+      if (n_pend == 1) {
+        tc::cp_async_wait<0>();
+        tc::fence_proxy_async();
+        arrive(U(C.a_full[pend_st0]));
+      }
+      arrive(U(C.plan_empty[s]));
+    }
+  } else {
+    // ---------------- epilogue (128 threads = TMEM lanes) ----------------
+    const int ep = tid - 256;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const float s_main =
+        ldexpf(1.f, -(tc::scale_exp(T.maxbits[0]) + tc::scale_exp(T.maxbits[1])));
+    const float s_corr = s_main * (1.f / (float)(1 << tc::LOG2_LO));
+    uint32_t cg = 0;
+    for (int64_t it = 0;; ++it) {
+      const int64_t t = blockIdx.x + it * gridDim.x;
+      if (t >= P.ntile) break;
+      const int64_t tile = P.tile0 + t;
+      const int s = (int)(it % NPL);
+      wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
+      const PlanSlot& S = C.slot[s];
+      const int n = S.n_cells;
+      const int n_chunks = (n + tc::M - 1) / tc::M;
+      for (int c = 0; c < n_chunks; ++c, ++cg) {
+        const int ab = cg & 1;
+        wait_full(U(C.acc_full[ab]), cg >> 1);
+        tc::tc_fence_after();
+        const int gi = c * tc::M + ep;
+        float* dst = nullptr;
+        int64_t plane = 0;
+        if (gi < n) {
+          const tc::CellRef cr = tc::cell_of(gi, S.plan, S.prefix, P.levels);
+          const int ch = P.ch[cr.level], cw = P.cw[cr.level];
+          plane = (int64_t)ch * cw * TQW;
+          dst = P.cache[cr.level] + tile * plane * TQH +
+                (int64_t)slot_of(cr.cy, cr.cx, ch, cw) * TQW;
+        }
+        float vm[32], vc[32];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          tc::tmem_ld32(tmem + ab * 128 + lane_base + h * 32, vm);
+          tc::tmem_ld32(tmem + ab * 128 + 64 + lane_base + h * 32, vc);
+          if (dst != nullptr) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              float4 o;
+              o.x = fmaf(vc[j + 0], s_corr, vm[j + 0] * s_main);
+              o.y = fmaf(vc[j + 1], s_corr, vm[j + 1] * s_main);
+              o.z = fmaf(vc[j + 2], s_corr, vm[j + 2] * s_main);
+              o.w = fmaf(vc[j + 3], s_corr, vm[j + 3] * s_main);
+              const int q = h * 32 + j;
+              *reinterpret_cast<float4*>(dst + (q >> 3) * plane + (q & 7)) = o;
+            }
+          }
+        }
+        tc::tc_fence_before();
+        arrive(U(C.acc_empty[ab]));
+      }
+      arrive(U(C.plan_empty[s]));
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+  }
+}
+
+size_t smem_bytes(int dp) {
+  return (size_t)NB * 2 * tc::N * dp * 2 + (size_t)NST * tc::A_STAGE + sizeof(Ctl) + 1024;
+}
+
+}  // namespace tcp
+
 }  // namespace cvb
 
 using namespace cvb;
@@ -508,6 +914,30 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
     if (used) CVB_REQUIRE(T.f2s[l], "partial_contract_tc: null level pointer");
   }
   if (T.P.ntile == 0) return CVB_OK;
+  static int persistent = -1;
+  if (persistent < 0) {
+    const char* e = getenv("CVB_TC_PERSISTENT");
+    persistent = (e == nullptr || e[0] != '0') ? 1 : 0;
+  }
+  if (persistent) {
+    static int n_sms = 0;
+    static bool attr_p = false;
+    if (n_sms == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const size_t smem = tcp::smem_bytes(T.dp);
+    if (!attr_p) {
+      cudaFuncSetAttribute(tcp::partial_contract_tcp_kernel,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tcp::smem_bytes(tc::MAX_DP));
+      attr_p = true;
+    }
+    const int64_t grid = T.P.ntile < n_sms ? T.P.ntile : n_sms;
+    tcp::partial_contract_tcp_kernel<<<(unsigned)grid, tcp::THREADS, smem, as_stream(stream)>>>(T);
+    return check_launch("partial_contract_tcp");
+  }
   const size_t smem = (size_t)2 * tc::N * T.dp * 2 + (size_t)tc::NST * tc::A_STAGE;
   static bool attr_set = false;
   if (!attr_set) {
