@@ -351,6 +351,9 @@ def main():
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
     sm_max = peaks.get("sm_max_mhz", 1965.0)
+    # dram bytes per launch from the committed `ncu --set full` capture (or null)
+    traffic_path = ROOT / "profiles" / f"ncu_traffic_{args.config}.json"
+    traffic = json.loads(traffic_path.read_text()) if traffic_path.exists() else {}
     geom_path = ROOT / "profiles" / f"geometry_{args.config}.json"
     geom = json.loads(geom_path.read_text()) if geom_path.exists() else None
     out_bytes_iter = rows * w * levels * k1 * k1 * 4
@@ -361,9 +364,10 @@ def main():
         tc, tg = sum(kern["contract_ms"]), sum(kern["gather_ms"])
         gather_bytes = (out_bytes_iter + coord_bytes_iter) * n_iter
         gather_gbs = gather_bytes / (tg / 1e3) / 1e9
-        r_gather = {"kernel": "partial_sample_kernel (gather/bilinear sampler)", "bound": "hbm",
+        r_gather = {"kernel": "gather_kernel (partial gather / bilinear sampler)", "bound": "hbm",
                     "achieved": round(gather_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
-                    "frac": round(gather_gbs / hbm_peak, 4), "traffic": None,
+                    "frac": round(gather_gbs / hbm_peak, 4),
+                    "traffic": traffic.get("gather_kernel"),
                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})",
                     "alg_bytes_per_launch": gather_bytes / n_iter,
                     "avg_launch_ms": tg / n_iter, "share_of_step": round(tg / (tc + tg), 3)}
@@ -377,7 +381,7 @@ def main():
                 src = ("MEASURED_PEAKS.json bf16_tflops_sustained (kind::f16 dense rate; "
                        "kernel timed inside the step)" if "bf16_tflops_sustained" in peaks
                        else "fallback 1.4 PFLOP/s sustained")
-                name = "partial_contract_tc_kernel (tiler + incremental tcgen05 contraction)"
+                name = "partial_contract_tcp_kernel (tiler + incremental tcgen05 contraction)"
                 bound = "tensor"
                 executed = 3 * 2 * d * kern["device_counters"]["dots"]
             else:
@@ -389,7 +393,9 @@ def main():
                 executed = 2 * d * kern["device_counters"]["dots"]
             r_con = {"kernel": name, "bound": bound, "achieved": round(tf, 2),
                      "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(tf / peak, 4),
-                     "traffic": None, "peak_source": src,
+                     "traffic": traffic.get("partial_contract_tcp_kernel" if kern["tensor_cores"]
+                                            else "partial_contract_kernel"),
+                     "peak_source": src,
                      "alg_flops_per_launch": flops / n_iter, "avg_launch_ms": tc / n_iter,
                      "share_of_step": round(tc / (tc + tg), 3),
                      "executed_flops": executed,
