@@ -98,7 +98,8 @@ int cvb_partial_sizes(const cvb_partial_desc* desc, int64_t* n_tiles, int64_t* m
   CVB_REQUIRE(desc->levels >= 1 && desc->levels <= CVB_MAX_LEVELS, "bad level count");
   const int64_t nt = ceil_div(desc->h1, TQH) * ceil_div(desc->w1, TQW);
   if (n_tiles) *n_tiles = nt;
-  if (meta_ints) *meta_ints = nt * desc->levels * CVB_META_INTS;
+  // per-level metadata, then one plan record per tile (tensor-core path)
+  if (meta_ints) *meta_ints = nt * desc->levels * CVB_META_INTS + nt * PLAN_INTS;
   if (cache_floats_per_level)
     for (int l = 0; l < desc->levels; ++l)
       cache_floats_per_level[l] = nt * (int64_t)desc->cap_h[l] * desc->cap_w[l] * TQ;
@@ -166,6 +167,7 @@ __attribute__((visibility("hidden"))) int cvb_internal_build_params(
   P.coords = coords;
   P.meta = meta;
   P.counters = counters;
+  P.plans = meta + ceil_div(desc->h1, TQH) * ceil_div(desc->w1, TQW) * desc->levels * CVB_META_INTS;
   P.tiles_x = (int)ceil_div(desc->w1, TQW);
   P.n_tiles = ceil_div(desc->h1, TQH) * (int64_t)P.tiles_x;
   P.scale = scale;

@@ -17,6 +17,7 @@ struct PartialParams {
   int th[CVB_MAX_LEVELS], tw[CVB_MAX_LEVELS], ch[CVB_MAX_LEVELS], cw[CVB_MAX_LEVELS];
   const void* coords;
   int32_t* meta;
+  int32_t* plans;        // PlanRec per tile (after the per-level meta, same buffer)
   unsigned long long* counters;
   int tiles_x;
   int64_t n_tiles;       // all tiles of the frame
@@ -79,6 +80,17 @@ struct TilePlan {
   Box B, I;
   int has_i, n_new, nvalid, status;
 };
+
+// All-level plan of one tile as the tensor-core contraction consumes it: one
+// 16-byte-aligned record per tile, copied into shared memory with one bulk
+// async copy (csrc/partial_tc.cu).
+struct alignas(16) PlanRec {
+  TilePlan plan[CVB_MAX_LEVELS];
+  int prefix[CVB_MAX_LEVELS + 1];  // cells of levels < l in the tile's new-cell list
+  int n_cells;
+  int pad[2];
+};
+constexpr int PLAN_INTS = (int)(sizeof(PlanRec) / 4);
 
 // Window-union tiler for one (tile, level); every thread of the CTA must call
 // it (blockDim >= 64).  Bounding box of the tile's (2r+2)^2 supports (offsets

@@ -3,11 +3,9 @@
 // Same tiler, metadata and toroidal tile cache as partial_contract_kernel
 // (partial.cuh); only the arithmetic of the new-cell contraction changes:
 //
-//   * one CTA per 8x8 query tile handles ALL levels: the new cells of every
-//     level are concatenated and contracted in chunks of 128 cells;
 //   * D[128 cells x 64 queries] = A[cells x K] . B[queries x K]^T with
 //     M=128, N=64, K=16 `tcgen05.mma.cta_group::1.kind::f16`, accumulators in
-//     TMEM (128 lanes x 64 fp32 columns, two of them);
+//     TMEM (a 2-deep ring of main + corr accumulators, 64 fp32 columns each);
 //   * split precision: every fp32 value x (pre-scaled by a per-tensor power of
 //     two so it sits in fp16 range) is stored as hi = fp16(x) and
 //     lo = fp16((x - hi) * 2^11); x*y = hi_x*hi_y + 2^-11 (hi_x*lo_y + lo_x*hi_y)
@@ -16,13 +14,17 @@
 //     tensor rate, well inside the fp32 tolerance (products of two fp16 are
 //     exact in the fp32 accumulator);
 //   * operands are pre-split once per image pair (cvb_tc_prepare): the F1
-//     tile is one contiguous 64 KB image of its shared-memory layout, fetched
-//     with a single bulk async copy (cp.async.bulk + mbarrier complete_tx);
-//     A rows (gathered bbox cells) stream through a 2-stage cp.async ring in
-//     the canonical K-major no-swizzle core-matrix layout (8 rows x 16 B);
+//     tile is a contiguous image of its shared-memory layout cut into K
+//     pieces of 64 channels (16 KB: hi 8 KB + lo 8 KB), each fetched with one
+//     bulk async copy (cp.async.bulk + mbarrier complete_tx) into a ring of
+//     pieces, so the next tile's first pieces land while the current tile's
+//     last chunk still runs; A rows (gathered new bbox cells of all levels,
+//     128 per chunk) stream through an 8-stage cp.async ring in the canonical
+//     K-major no-swizzle core-matrix layout (8 rows x 16 B) that never drains
+//     between tiles;
 //   * the epilogue reads TMEM with tcgen05.ld, combines main + 2^-11 corr,
 //     removes the power-of-two scales and writes each cell's 64 query costs
-//     (256 contiguous bytes) into its cache slot.
+//     into its cache slot.
 #include <cuda_fp16.h>
 #include <stdlib.h>
 
@@ -31,13 +33,13 @@
 namespace cvb {
 namespace tc {
 
-constexpr int THREADS = 128;
 constexpr int M = 128;         // cells per MMA chunk (TMEM lanes)
 constexpr int N = 64;          // queries per tile
-constexpr int KS = 32;         // K per pipeline stage
-constexpr int NST = 2;         // pipeline stages
-constexpr int A_HALF = M * KS * 2;       // 8 KB (hi or lo)
-constexpr int A_STAGE = 2 * A_HALF;      // 16 KB
+constexpr int KP = 64;         // K per A stage and per B piece (one 128-byte swizzle atom row)
+constexpr int A_HALF = M * KP * 2;       // 16 KB (hi or lo)
+constexpr int A_STAGE = 2 * A_HALF;      // 32 KB
+constexpr int B_HALF = N * KP * 2;       // 8 KB (hi or lo)
+constexpr int B_PIECE = 2 * B_HALF;      // 16 KB
 constexpr int MAX_DP = 256;
 constexpr int LOG2_LO = 11;              // lo part scale
 constexpr int TARGET_EXP = 14;           // max |x * 2^e| < 2^14
@@ -58,6 +60,19 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;
+  return d;
+}
+
+// K-major, SWIZZLE_128B descriptor: rows of 128 B (64 fp16 of K) in 8-row,
+// 1024-byte atoms (the layout TMA writes with CU_TENSOR_MAP_SWIZZLE_128B);
+// SBO = 1024 B between 8-row groups; a K=16 step advances the start by 32 B.
+__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
   return d;
 }
 
@@ -170,6 +185,7 @@ struct TcParams {
   int64_t plane[CVB_MAX_LEVELS];
   const uint32_t* maxbits;             // [0] max|F1|, [1] max|F2|
   int dp;
+  int dbg;                             // profiling knockouts (CVB_TC_DEBUG), 0 in production
 };
 
 __global__ void absmax_kernel(const float* __restrict__ x, int64_t n, uint32_t* out) {
@@ -182,13 +198,15 @@ __global__ void absmax_kernel(const float* __restrict__ x, int64_t n, uint32_t* 
   if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
 }
 
-// F1 -> per-tile image of the B operand: [2][8 rowgroups][dp/8][8 rows][8]
+// F1 -> per-tile image of the B operand, cut into K pieces of KP channels:
+// [dp/KP pieces][hi, lo][8 row groups][KP/8 k groups][8 rows][8 channels] fp16
 __global__ void split_f1_kernel(const float* __restrict__ f1, int h1, int w1, int d, int dp,
                                 int tiles_x, int64_t n_tiles, const uint32_t* maxbits,
                                 uint8_t* __restrict__ out) {
   const int kgs = dp / 8;
   const int64_t total = n_tiles * N * kgs;
   const float s = ldexpf(1.f, scale_exp(maxbits[0]));
+  const int64_t tile_bytes = (int64_t)N * dp * 2 * 2;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int kg = (int)(i % kgs);
@@ -203,10 +221,11 @@ __global__ void split_f1_kernel(const float* __restrict__ f1, int h1, int w1, in
     }
     uint4 hi, lo;
     split8(x, s, hi, lo);
-    const int64_t half_bytes = (int64_t)N * dp * 2;
-    uint8_t* base = out + tile * 2 * half_bytes + (q / 8) * (kgs * 128) + kg * 128 + (q % 8) * 16;
+    const int piece = kg / (KP / 8), kgi = kg % (KP / 8);
+    uint8_t* base = out + tile * tile_bytes + (int64_t)piece * B_PIECE + (q / 8) * (KP / 8 * 128) +
+                    kgi * 128 + (q % 8) * 16;
     *reinterpret_cast<uint4*>(base) = hi;
-    *reinterpret_cast<uint4*>(base + half_bytes) = lo;
+    *reinterpret_cast<uint4*>(base + B_HALF) = lo;
   }
 }
 
@@ -237,6 +256,7 @@ struct CellRef {
   int level, cy, cx;
 };
 
+// g-th row of a tile's new-cell list (levels concatenated).
 __device__ __forceinline__ CellRef cell_of(int g, const TilePlan* plans, const int* prefix,
                                            int levels) {
   int l = 0;
@@ -247,230 +267,43 @@ __device__ __forceinline__ CellRef cell_of(int g, const TilePlan* plans, const i
   return c;
 }
 
-__global__ void __launch_bounds__(THREADS) partial_contract_tc_kernel(TcParams T) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bars[NST + 2];  // stage_free[NST], acc_full, b_full
-  __shared__ uint32_t s_tmem;
-  __shared__ TilePlan s_plan[CVB_MAX_LEVELS];
-  __shared__ int s_red[CVB_MAX_LEVELS][2][4];
-  __shared__ int s_nvalid;
-  __shared__ int s_prefix[CVB_MAX_LEVELS + 1];
-
-  const PartialParams& P = T.P;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int64_t tile = P.tile0 + blockIdx.x;
-  const int dp = T.dp;
-  const uint32_t half_bytes = (uint32_t)N * dp * 2;  // one of hi / lo
-  const uint32_t b_bytes = 2 * half_bytes;
-  const uint32_t sB = smem_u32(smem);
-  const uint32_t sA = sB + b_bytes;
-  const uint32_t bar_stage = smem_u32(&bars[0]);
-  const uint32_t bar_acc = smem_u32(&bars[NST]);
-  const uint32_t bar_b = smem_u32(&bars[NST + 1]);
-
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
-                     smem_u32(&s_tmem))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  if (tid == 32) {
-    s_nvalid = 0;
-    for (int i = 0; i < NST + 2; ++i) mbar_init(bar_stage + 8 * i, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = s_tmem;
-  const uint32_t d_main = tmem, d_corr = tmem + 64;
-
-  // B operand: the pre-split F1 tile image, one bulk async copy
-  if (tid == 0) {
-    mbar_expect_tx(bar_b, b_bytes);
-    const uint8_t* src = T.f1s + tile * (int64_t)b_bytes;
-    const uint32_t piece = b_bytes / 4;
-    for (int i = 0; i < 4; ++i) bulk_g2s(sB + i * piece, src + i * piece, piece, bar_b);
-  }
-
-  // window-union tiler for every level (overlaps the B copy)
-  plan_tile_all_levels(P, tile, s_plan, s_red, &s_nvalid);
-  if (tid == 0) {
-    s_prefix[0] = 0;
-    for (int l = 0; l < P.levels; ++l) s_prefix[l + 1] = s_prefix[l] + s_plan[l].n_new;
-  }
-  __syncthreads();
-  const int n_cells = s_prefix[P.levels];
-  const int n_chunks = (n_cells + M - 1) / M;
-  const int n_ks = dp / KS;
-  const int n_steps = n_chunks * n_ks;
-
-  const int rg = tid >> 3, r8 = tid & 7;
-  const uint32_t row_off = rg * (KS / 8) * 128 + r8 * 16;  // A: SBO = 512 B
-  int load_chunk = -1;
-  const __half* src_hi = nullptr;
-  const __half* src_lo = nullptr;
-
-  auto issue_loads = [&](int c, int ks, int st) {
-    if (c != load_chunk) {
-      load_chunk = c;
-      src_hi = nullptr;
-      const int g = c * M + tid;
-      if (g < n_cells) {
-        const CellRef cr = cell_of(g, s_plan, s_prefix, P.levels);
-        src_hi = T.f2s[cr.level] + ((int64_t)cr.cy * P.tw[cr.level] + cr.cx) * dp;
-        src_lo = src_hi + T.plane[cr.level];
-      }
-    }
-    if (src_hi != nullptr) {
-      const uint32_t dst = sA + st * A_STAGE + row_off;
-#pragma unroll
-      for (int j = 0; j < KS / 8; ++j) {
-        cp_async16(dst + j * 128, src_hi + ks * KS + j * 8);
-        cp_async16(dst + A_HALF + j * 128, src_lo + ks * KS + j * 8);
-      }
-    }
-    cp_async_commit();
-  };
-
-  if (n_steps > 0) issue_loads(0, 0, 0);
-  if (tid == 0) mbar_wait(bar_b, 0);
-  const float s_main = ldexpf(1.f, -(scale_exp(T.maxbits[0]) + scale_exp(T.maxbits[1])));
-  const float s_corr = s_main * (1.f / (float)(1 << LOG2_LO));
-
-  // step i = (chunk c, k-slice ks) uses stage st = i % NST; its n-th use
-  // (n = i / NST) completes phase n of stage_free[st]
-  int c = 0, ks = 0, st = 0;
-  int nc = 0, nks = 1, nst = 1 % NST, nuse = (1 >= NST) ? 1 : 0;  // next step, stage use count
-  if (nks == n_ks) {
-    nks = 0;
-    ++nc;
-  }
-  for (int i = 0; i < n_steps; ++i) {
-    if (i + 1 < n_steps) {
-      if (i + 1 >= NST) mbar_wait(bar_stage + 8 * nst, (nuse - 1) & 1);
-      issue_loads(nc, nks, nst);
-      cp_async_wait<1>();
-      if (++nks == n_ks) {
-        nks = 0;
-        ++nc;
-      }
-      if (++nst == NST) {
-        nst = 0;
-        ++nuse;
-      }
-    } else {
-      cp_async_wait<0>();
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      const uint32_t a_hi = sA + st * A_STAGE, a_lo = a_hi + A_HALF;
-#pragma unroll
-      for (int s = 0; s < KS / 16; ++s) {
-        const uint32_t kstep = ks * (KS / 16) + s;
-        const uint64_t dah = make_desc(a_hi + s * 256, 128, (KS / 8) * 128);
-        const uint64_t dal = make_desc(a_lo + s * 256, 128, (KS / 8) * 128);
-        const uint64_t dbh = make_desc(sB + kstep * 256, 128, (dp / 8) * 128);
-        const uint64_t dbl = make_desc(sB + half_bytes + kstep * 256, 128, (dp / 8) * 128);
-        const uint32_t acc = (ks > 0 || s > 0) ? 1u : 0u;
-        mma_f16(d_main, dah, dbh, acc);
-        mma_f16(d_corr, dah, dbl, acc);
-        mma_f16(d_corr, dal, dbh, 1u);
-      }
-      mma_commit(bar_stage + 8 * st);
-      if (ks == n_ks - 1) mma_commit(bar_acc);
-    }
-    if (ks == n_ks - 1) {
-      // ---- epilogue of chunk c ----
-      mbar_wait(bar_acc, c & 1);
-      tc_fence_after();
-      const int g = c * M + tid;
-      const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-      float vm[32], vc[32];
-      float* dst = nullptr;  // tile block of the cell's level: [query row][slot][8]
-      int64_t plane = 0, slot = 0;
-      if (g < n_cells) {
-        const CellRef cr = cell_of(g, s_plan, s_prefix, P.levels);
-        const int ch = P.ch[cr.level], cw = P.cw[cr.level];
-        plane = (int64_t)ch * cw * TQW;
-        slot = slot_of(cr.cy, cr.cx, ch, cw);
-        dst = P.cache[cr.level] + tile * plane * TQH + slot * TQW;
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        tmem_ld32(d_main + lane_base + h * 32, vm);
-        tmem_ld32(d_corr + lane_base + h * 32, vc);
-        if (dst != nullptr) {
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            float4 o;
-            o.x = fmaf(vc[j + 0], s_corr, vm[j + 0] * s_main);
-            o.y = fmaf(vc[j + 1], s_corr, vm[j + 1] * s_main);
-            o.z = fmaf(vc[j + 2], s_corr, vm[j + 2] * s_main);
-            o.w = fmaf(vc[j + 3], s_corr, vm[j + 3] * s_main);
-            const int q = h * 32 + j;  // queries q..q+3 share query row q/8
-            *reinterpret_cast<float4*>(dst + (q >> 3) * plane + (q & 7)) = o;
-          }
-        }
-      }
-      tc_fence_before();
-      __syncthreads();
-    }
-    if (++ks == n_ks) {
-      ks = 0;
-      ++c;
-    }
-    if (++st == NST) st = 0;
-  }
-  if (n_steps == 0 && tid == 0) mbar_wait(bar_b, 0);
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
-  }
-}
-
 }  // namespace tc
 
 // ---------------------------------------------------------------------------
-// Persistent, warp-specialised variant (default).  One CTA per SM walks the
-// tiles blockIdx.x, blockIdx.x + gridDim.x, ...; the roles communicate only
-// through mbarrier rings, so the next tile's planning, B image and A rows are
-// in flight while the current tile's MMAs run and the previous chunk's
-// accumulators drain:
-//   warp 0       B producer: one 64 KB bulk copy per tile into a 2-deep ring
+// Persistent, warp-specialised contraction.  One CTA per SM walks the tiles
+// blockIdx.x, blockIdx.x + gridDim.x, ...; the roles communicate only through
+// mbarrier rings, so the next tile's plan, F1 pieces and A rows are in flight
+// while the current tile's MMAs run and the previous chunk's accumulators
+// drain.  No thread ever waits on its own copy (bulk copies complete_tx,
+// cp.async arrive-on-completion):
+//   warp 0       B producer: one 16 KB bulk copy per F1 K-piece into an
+//                NBP-deep piece ring (a piece is released after the last
+//                chunk of its tile has consumed it)
 //   warp 1       MMA issuer (one thread): 3 tcgen05.mma per K=16 step
-//   warps 2-3    planner: the window-union tiler for every level of a tile
-//   warps 4-7    A producers: one A row (cell) per thread, cp.async into a
-//                4-stage ring, fence.proxy.async + arrive once a stage landed
+//   warp 2       plan loader: the tile's PlanRec (window-union tiler output
+//                of every level, computed for all tiles at once by
+//                plan_kernel) via one bulk copy into an NPL-deep slot ring
+//   warps 4-7    A producers: per chunk and 64-channel K block, every new
+//                cell's hi and lo 128-byte rows via cp.async (full L2 lines)
+//                into a 128B-swizzled NST-stage ring, completion tracked by
+//                cp.async.mbarrier.arrive.noinc
 //   warps 8-11   epilogue: tcgen05.ld of a 2-deep TMEM accumulator ring,
 //                main + 2^-11 corr, cache-slot stores
 // ---------------------------------------------------------------------------
 namespace tcp {
 
-constexpr int NST = 4;   // A stages
-constexpr int NB = 2;    // B buffers
-constexpr int NPL = 4;   // plan slots (the planner runs up to 3 tiles ahead)
+constexpr int NST = 4;              // A stages (32 KB each: hi + lo, 128 rows x 64 channels)
+constexpr int NBP = 5;              // F1 pieces in the ring (16 KB each)
+constexpr int NPL = 4;              // plan slots
 constexpr int THREADS = 384;
 constexpr uint32_t SPIN_LIMIT = 1u << 24;  // watchdog: trap instead of hanging
 
-struct PlanSlot {
-  TilePlan plan[CVB_MAX_LEVELS];
-  int prefix[CVB_MAX_LEVELS + 1];
-  int n_cells;
-};
-
 struct Ctl {
   uint64_t plan_full[NPL], plan_empty[NPL];
-  uint64_t b_full[NB], b_empty[NB];
+  uint64_t b_full[NBP], b_empty[NBP];
   uint64_t a_full[NST], a_empty[NST];
   uint64_t acc_full[2], acc_empty[2];
-  PlanSlot slot[NPL];
-  int red[CVB_MAX_LEVELS][2][4];
-  int nv[2];
+  PlanRec slot[NPL];
   uint32_t tmem;
 };
 
@@ -499,22 +332,21 @@ __device__ __forceinline__ void wait_empty(uint32_t bar, uint32_t k) {
 __device__ __forceinline__ void arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void named_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 
-__global__ void __launch_bounds__(THREADS, 1) partial_contract_tcp_kernel(tc::TcParams T) {
-  extern __shared__ __align__(1024) uint8_t smem[];
+__global__ void __launch_bounds__(THREADS, 1)
+    partial_contract_tcp_kernel(const __grid_constant__ tc::TcParams T) {
+  extern __shared__ uint8_t smem_raw[];
   const PartialParams& P = T.P;
   const int dp = T.dp;
-  const uint32_t half_bytes = (uint32_t)tc::N * dp * 2;
-  const uint32_t b_bytes = 2 * half_bytes;
-  uint8_t* sB = smem;                                   // NB x b_bytes
-  uint8_t* sA = smem + NB * b_bytes;                    // NST x A_STAGE
-  Ctl& C = *reinterpret_cast<Ctl*>(sA + NST * tc::A_STAGE);
+  const int n_kb = dp / tc::KP;  // K blocks = A stages per chunk = F1 pieces per tile
+  // 1024-byte alignment for the 128B-swizzled A stages
+  const uint32_t raw = tc::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint8_t* sA = smem;                        // NST x A_STAGE
+  uint8_t* sB = smem + NST * tc::A_STAGE;    // NBP x B_PIECE
+  Ctl& C = *reinterpret_cast<Ctl*>(sB + NBP * tc::B_PIECE);
   const uint32_t uB = tc::smem_u32(sB), uA = tc::smem_u32(sA);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n_ks = dp / tc::KS;
   auto U = [](const uint64_t& b) { return tc::smem_u32(&b); };
 
   if (warp == 0) {
@@ -525,10 +357,10 @@ __global__ void __launch_bounds__(THREADS, 1) partial_contract_tcp_kernel(tc::Tc
   }
   if (tid == 32) {
     for (int i = 0; i < NPL; ++i) {
-      tc::mbar_init(U(C.plan_full[i]), 64);
+      tc::mbar_init(U(C.plan_full[i]), 1);
       tc::mbar_init(U(C.plan_empty[i]), 1 + 1 + 128 + 128);
     }
-    for (int i = 0; i < NB; ++i) {
+    for (int i = 0; i < NBP; ++i) {
       tc::mbar_init(U(C.b_full[i]), 1);
       tc::mbar_init(U(C.b_empty[i]), 1);
     }
@@ -548,23 +380,27 @@ __global__ void __launch_bounds__(THREADS, 1) partial_contract_tcp_kernel(tc::Tc
   const uint32_t tmem = C.tmem;
 
   if (warp == 0) {
-    // ---------------- B producer ----------------
+    // ---------------- B producer: F1 pieces ----------------
     if (lane == 0) {
-      uint32_t kb = 0;
+      uint32_t pb = 0;  // pieces issued so far
       for (int64_t it = 0;; ++it) {
         const int64_t t = blockIdx.x + it * gridDim.x;
         if (t >= P.ntile) break;
         const int s = (int)(it % NPL);
         wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
         if (C.slot[s].n_cells > 0) {
-          const int tb = kb % NB;
-          wait_empty(U(C.b_empty[tb]), kb / NB);
-          tc::mbar_expect_tx(U(C.b_full[tb]), b_bytes);
-          const uint8_t* src = T.f1s + (P.tile0 + t) * (int64_t)b_bytes;
-          const uint32_t piece = b_bytes / 4;
-          for (int i = 0; i < 4; ++i)
-            tc::bulk_g2s(uB + tb * b_bytes + i * piece, src + i * piece, piece, U(C.b_full[tb]));
-          ++kb;
+          const uint8_t* src = T.f1s + (P.tile0 + t) * (int64_t)n_kb * tc::B_PIECE;
+          for (int q = 0; q < n_kb; ++q, ++pb) {
+            const int bs = (int)(pb % NBP);
+            wait_empty(U(C.b_empty[bs]), pb / NBP);
+            if (T.dbg & 8) {
+              arrive(U(C.b_full[bs]));
+              continue;
+            }
+            tc::mbar_expect_tx(U(C.b_full[bs]), tc::B_PIECE);
+            tc::bulk_g2s(uB + bs * tc::B_PIECE, src + (int64_t)q * tc::B_PIECE, tc::B_PIECE,
+                         U(C.b_full[bs]));
+          }
         }
         arrive(U(C.plan_empty[s]));
       }
@@ -572,7 +408,7 @@ __global__ void __launch_bounds__(THREADS, 1) partial_contract_tcp_kernel(tc::Tc
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      uint32_t kb = 0, g = 0, cg = 0;
+      uint32_t pb = 0, g = 0, cg = 0;
       for (int64_t it = 0;; ++it) {
         const int64_t t = blockIdx.x + it * gridDim.x;
         if (t >= P.ntile) break;
@@ -580,197 +416,115 @@ __global__ void __launch_bounds__(THREADS, 1) partial_contract_tcp_kernel(tc::Tc
         wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
         const int n = C.slot[s].n_cells;
         if (n > 0) {
-          const int tb = kb % NB;
-          wait_full(U(C.b_full[tb]), kb / NB);
-          const uint32_t bh = uB + tb * b_bytes, bl = bh + half_bytes;
           const int n_chunks = (n + tc::M - 1) / tc::M;
           for (int c = 0; c < n_chunks; ++c, ++cg) {
             const int ab = cg & 1;
             wait_empty(U(C.acc_empty[ab]), cg >> 1);
             tc::tc_fence_after();
             const uint32_t d_main = tmem + ab * 128, d_corr = d_main + 64;
-            for (int ks = 0; ks < n_ks; ++ks, ++g) {
-              const int st = g % NST;
+            for (int kb = 0; kb < n_kb; ++kb, ++g) {
+              const uint32_t pi = pb + kb;
+              const int bs = (int)(pi % NBP);
+              if (c == 0) wait_full(U(C.b_full[bs]), pi / NBP);
+              const int st = (int)(g % NST);
               wait_full(U(C.a_full[st]), g / NST);
               tc::tc_fence_after();
               const uint32_t a_hi = uA + st * tc::A_STAGE, a_lo = a_hi + tc::A_HALF;
+              const uint32_t b_hi = uB + bs * tc::B_PIECE, b_lo = b_hi + tc::B_HALF;
+              if (!(T.dbg & 4)) {
 #pragma unroll
-              for (int k2 = 0; k2 < tc::KS / 16; ++k2) {
-                const uint32_t kstep = ks * (tc::KS / 16) + k2;
-                const uint64_t dah = tc::make_desc(a_hi + k2 * 256, 128, (tc::KS / 8) * 128);
-                const uint64_t dal = tc::make_desc(a_lo + k2 * 256, 128, (tc::KS / 8) * 128);
-                const uint64_t dbh = tc::make_desc(bh + kstep * 256, 128, (dp / 8) * 128);
-                const uint64_t dbl = tc::make_desc(bl + kstep * 256, 128, (dp / 8) * 128);
-                const uint32_t acc = (ks > 0 || k2 > 0) ? 1u : 0u;
-                tc::mma_f16(d_main, dah, dbh, acc);
-                tc::mma_f16(d_corr, dah, dbl, acc);
-                tc::mma_f16(d_corr, dal, dbh, 1u);
+                for (int k = 0; k < tc::KP / 16; ++k) {
+                  const uint64_t dah = tc::make_desc_sw128(a_hi + k * 32);
+                  const uint64_t dal = tc::make_desc_sw128(a_lo + k * 32);
+                  const uint64_t dbh = tc::make_desc(b_hi + k * 256, 128, (tc::KP / 8) * 128);
+                  const uint64_t dbl = tc::make_desc(b_lo + k * 256, 128, (tc::KP / 8) * 128);
+                  const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+                  tc::mma_f16(d_main, dah, dbh, acc);
+                  tc::mma_f16(d_corr, dah, dbl, acc);
+                  tc::mma_f16(d_corr, dal, dbh, 1u);
+                }
               }
               tc::mma_commit(U(C.a_empty[st]));
+              if (c == n_chunks - 1) tc::mma_commit(U(C.b_empty[bs]));
             }
             tc::mma_commit(U(C.acc_full[ab]));
           }
-          tc::mma_commit(U(C.b_empty[tb]));
-          ++kb;
+          pb += n_kb;
         }
         arrive(U(C.plan_empty[s]));
       }
     }
-  } else if (warp < 4) {
-    // ---------------- planner (64 threads) ----------------
-    const int pt = tid - 64, pw = pt >> 5;
-    const int r = P.radius;
-    for (int64_t it = 0;; ++it) {
-      const int64_t t = blockIdx.x + it * gridDim.x;
-      if (t >= P.ntile) break;
-      const int64_t tile = P.tile0 + t;
-      const int s = (int)(it % NPL);
-      wait_empty(U(C.plan_empty[s]), (uint32_t)(it / NPL));
-      const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
-      const int py = tile_y * TQH + pt / TQW, px = tile_x * TQW + pt % TQW;
-      const bool valid = py < P.h1 && px < P.w1;
-      double x = 0.0, y = 0.0;
-      if (valid) load_coord(P.coords, P.f64, (int64_t)py * P.w1 + px, x, y);
-      const unsigned vote = __ballot_sync(0xffffffffu, valid);
-      if (lane == 0) C.nv[pw] = __popc(vote);
-      for (int l = 0; l < P.levels; ++l) {
-        int ylo = INT_MAX, yhi = INT_MIN, xlo = INT_MAX, xhi = INT_MIN;
-        if (valid) {
-          const LevelPos lp = level_pos(x, y, l);
-          ylo = yhi = clamp_anchor(lp.y0, r, P.th[l]);
-          xlo = xhi = clamp_anchor(lp.x0, r, P.tw[l]);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          ylo = min(ylo, __shfl_xor_sync(0xffffffffu, ylo, o));
-          yhi = max(yhi, __shfl_xor_sync(0xffffffffu, yhi, o));
-          xlo = min(xlo, __shfl_xor_sync(0xffffffffu, xlo, o));
-          xhi = max(xhi, __shfl_xor_sync(0xffffffffu, xhi, o));
-        }
-        if (lane == 0) {
-          C.red[l][pw][0] = ylo;
-          C.red[l][pw][1] = yhi;
-          C.red[l][pw][2] = xlo;
-          C.red[l][pw][3] = xhi;
-        }
+  } else if (warp == 2) {
+    // ---------------- plan loader: one bulk copy per tile record ----------------
+    if (lane == 0) {
+      for (int64_t it = 0;; ++it) {
+        const int64_t t = blockIdx.x + it * gridDim.x;
+        if (t >= P.ntile) break;
+        const int s = (int)(it % NPL);
+        wait_empty(U(C.plan_empty[s]), (uint32_t)(it / NPL));
+        tc::mbar_expect_tx(U(C.plan_full[s]), (uint32_t)sizeof(PlanRec));
+        tc::bulk_g2s(tc::smem_u32(&C.slot[s]), P.plans + (P.tile0 + t) * PLAN_INTS,
+                     (uint32_t)sizeof(PlanRec), U(C.plan_full[s]));
       }
-      named_sync(1, 64);
-      PlanSlot& S = C.slot[s];
-      if (pt < P.levels) {
-        const int level = pt;
-        const int th = P.th[level], tw = P.tw[level];
-        int32_t* meta = P.meta + (tile * P.levels + level) * CVB_META_INTS;
-        const int nv = C.nv[0] + C.nv[1];
-        Box B;
-        B.ylo = max(min(C.red[level][0][0], C.red[level][1][0]) - r, 0);
-        B.yhi = min(max(C.red[level][0][1], C.red[level][1][1]) + r + 1, th - 1);
-        B.xlo = max(min(C.red[level][0][2], C.red[level][1][2]) - r, 0);
-        B.xhi = min(max(C.red[level][0][3], C.red[level][1][3]) + r + 1, tw - 1);
-        int status = ST_OK;
-        if (nv == 0 || B.empty()) {
-          status = ST_EMPTY;
-          B = Box{1, 0, 1, 0};
-        } else if (B.h() > P.ch[level] || B.w() > P.cw[level]) {
-          status = ST_OVERFLOW;
-        }
-        const Box prev{meta[0], meta[1], meta[2], meta[3]};
-        const bool prev_ok = !P.no_cache && meta[4] == ST_OK && !prev.empty();
-        const Box I{max(B.ylo, prev.ylo), min(B.yhi, prev.yhi), max(B.xlo, prev.xlo),
-                    min(B.xhi, prev.xhi)};
-        const bool has_i = status == ST_OK && prev_ok && !I.empty();
-        const int n_new = status == ST_OK ? (int)(B.area() - (has_i ? I.area() : 0)) : 0;
-        S.plan[level] = TilePlan{B, I, (int)has_i, n_new, nv, status};
-        meta[0] = B.ylo;
-        meta[1] = B.yhi;
-        meta[2] = B.xlo;
-        meta[3] = B.xhi;
-        meta[4] = status;
-        meta[5] = n_new;
-        if (P.counters != nullptr) {
-          if (n_new > 0) {
-            atomicAdd(P.counters + 0, (unsigned long long)n_new * nv);
-            atomicAdd(P.counters + 1, (unsigned long long)n_new);
-          }
-          if (status == ST_OVERFLOW) atomicAdd(P.counters + 2, 1ULL);
-          if (status == ST_EMPTY) atomicAdd(P.counters + 3, 1ULL);
-        }
-      }
-      named_sync(1, 64);
-      if (pt == 0) {
-        S.prefix[0] = 0;
-        for (int l = 0; l < P.levels; ++l) S.prefix[l + 1] = S.prefix[l] + S.plan[l].n_new;
-        S.n_cells = S.prefix[P.levels];
-      }
-      named_sync(1, 64);
-      arrive(U(C.plan_full[s]));
     }
-  } else if (warp < 8) {
-    // ---------------- A producers (128 threads, one A row each) ----------------
-    const int ap = tid - 128;
-    const uint32_t row_off = (ap >> 3) * (tc::KS / 8) * 128 + (ap & 7) * 16;
-    uint32_t g = 0;
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- A producers: cp.async of the new cells ----------------
+    // warp aw owns A rows 32aw..32aw+31; per 4-row group one warp instruction
+    // moves 4 full 128-byte rows (8 lanes x 16 B each, full L2 lines) into
+    // the 128B-swizzled stage; completion is signalled per thread with
+    // cp.async.mbarrier.arrive.noinc, so no producer thread ever waits on
+    // its own copies.
+    const int aw = warp - 4;
+    const int sub = lane >> 3, chunk = lane & 7;
+    uint32_t g = 0;  // A stages issued
     for (int64_t it = 0;; ++it) {
       const int64_t t = blockIdx.x + it * gridDim.x;
       if (t >= P.ntile) break;
       const int s = (int)(it % NPL);
       wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
-      const PlanSlot& S = C.slot[s];
+      const PlanRec& S = C.slot[s];
       const int n = S.n_cells;
       const int n_chunks = (n + tc::M - 1) / tc::M;
-      // stages issued but not yet published (at most NST-1 in flight)
-      int n_pend = 0;
-      uint32_t pend_st0 = 0, pend_st1 = 0;
       for (int c = 0; c < n_chunks; ++c) {
-        const __half* src_hi = nullptr;
-        const __half* src_lo = nullptr;
-        const int gi = c * tc::M + ap;
+        // source row of A row 32aw + lane (hi plane; lo = hi + plane)
+        const int gi = c * tc::M + 32 * aw + lane;
+        const __half* my_hi = nullptr;
+        int64_t my_plane = 0;
         if (gi < n) {
           const tc::CellRef cr = tc::cell_of(gi, S.plan, S.prefix, P.levels);
-          src_hi = T.f2s[cr.level] + ((int64_t)cr.cy * P.tw[cr.level] + cr.cx) * dp;
-          src_lo = src_hi + T.plane[cr.level];
+          my_hi = T.f2s[cr.level] + ((int64_t)cr.cy * P.tw[cr.level] + cr.cx) * dp;
+          my_plane = T.plane[cr.level];
         }
-        for (int ks = 0; ks < n_ks; ++ks, ++g) {
-          const int st = g % NST;
+        for (int kb = 0; kb < n_kb; ++kb, ++g) {
+          const int st = (int)(g % NST);
           wait_empty(U(C.a_empty[st]), g / NST);
-          if (src_hi != nullptr) {
-            const uint32_t dst = uA + st * tc::A_STAGE + row_off;
+          if (!(T.dbg & 1)) {
+            const uint32_t stage = uA + st * tc::A_STAGE;
 #pragma unroll
-            for (int j = 0; j < tc::KS / 8; ++j) {
-              tc::cp_async16(dst + j * 128, src_hi + ks * tc::KS + j * 8);
-              tc::cp_async16(dst + tc::A_HALF + j * 128, src_lo + ks * tc::KS + j * 8);
+            for (int i = 0; i < 8; ++i) {
+              const int rl = 4 * i + sub;  // row within the warp's 32
+              const __half* hi = reinterpret_cast<const __half*>(
+                  __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_hi), rl));
+              const int64_t pl = __shfl_sync(0xffffffffu, my_plane, rl);
+              if (hi != nullptr) {
+                const int row = 32 * aw + rl;
+                const uint32_t dst = stage + row * 128 + ((chunk ^ (row & 7)) << 4);
+                const __half* src = hi + kb * tc::KP + chunk * 8;
+                tc::cp_async16(dst, src);
+                tc::cp_async16(dst + tc::A_HALF, src + pl);
+              }
             }
-          }
-          tc::cp_async_commit();
-          if (n_pend == 2) {  // the oldest stage landed: publish it to the tensor core
-            tc::cp_async_wait<2>();
-            tc::fence_proxy_async();
-            arrive(U(C.a_full[pend_st0]));
-            pend_st0 = pend_st1;
-            pend_st1 = st;
-          } else if (n_pend == 1) {
-            pend_st1 = st;
-            n_pend = 2;
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                             U(C.a_full[st]))
+                         : "memory");
           } else {
-            pend_st0 = st;
-            n_pend = 1;
+            arrive(U(C.a_full[st]));
           }
         }
-      }
-      if (n_pend == 2) {
-        tc::cp_async_wait<1>();
-        tc::fence_proxy_async();
-        arrive(U(C.a_full[pend_st0]));
-        pend_st0 = pend_st1;
-        n_pend = 1;
-      }
-      if (n_pend == 1) {
-        tc::cp_async_wait<0>();
-        tc::fence_proxy_async();
-        arrive(U(C.a_full[pend_st0]));
       }
       arrive(U(C.plan_empty[s]));
     }
-  } else {
+  } else if (warp >= 8) {
     // ---------------- epilogue (128 threads = TMEM lanes) ----------------
     const int ep = tid - 256;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
@@ -784,7 +538,7 @@ __global__ void __launch_bounds__(THREADS, 1) partial_contract_tcp_kernel(tc::Tc
       const int64_t tile = P.tile0 + t;
       const int s = (int)(it % NPL);
       wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
-      const PlanSlot& S = C.slot[s];
+      const PlanRec& S = C.slot[s];
       const int n = S.n_cells;
       const int n_chunks = (n + tc::M - 1) / tc::M;
       for (int c = 0; c < n_chunks; ++c, ++cg) {
@@ -806,7 +560,7 @@ __global__ void __launch_bounds__(THREADS, 1) partial_contract_tcp_kernel(tc::Tc
         for (int h = 0; h < 2; ++h) {
           tc::tmem_ld32(tmem + ab * 128 + lane_base + h * 32, vm);
           tc::tmem_ld32(tmem + ab * 128 + 64 + lane_base + h * 32, vc);
-          if (dst != nullptr) {
+          if (dst != nullptr && !(T.dbg & 2)) {
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
               float4 o;
@@ -833,8 +587,133 @@ __global__ void __launch_bounds__(THREADS, 1) partial_contract_tcp_kernel(tc::Tc
   }
 }
 
-size_t smem_bytes(int dp) {
-  return (size_t)NB * 2 * tc::N * dp * 2 + (size_t)NST * tc::A_STAGE + sizeof(Ctl) + 1024;
+// Window-union tiler for every tile and level of the range, one warp per
+// tile (two queries per lane; per-level bounding boxes by warp shuffles; lane
+// l finalises level l against its previous box in meta), eight tiles per CTA.
+// Writes the tile's PlanRec for the persistent contraction and updates the
+// per-level meta; the work counters are reduced per CTA (one atomic each).
+constexpr int PLAN_WARPS = 8;
+
+__global__ void __launch_bounds__(PLAN_WARPS * 32) plan_kernel(PartialParams P) {
+  __shared__ unsigned long long s_cnt[4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0ULL;
+  __syncthreads();
+  const int64_t t = (int64_t)blockIdx.x * PLAN_WARPS + warp;
+  if (t < P.ntile) {
+    const int64_t tile = P.tile0 + t;
+    const int r = P.radius;
+    const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
+    double x[2], y[2];
+    bool v[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = lane + 32 * h;
+      const int py = tile_y * TQH + q / TQW, px = tile_x * TQW + q % TQW;
+      v[h] = py < P.h1 && px < P.w1;
+      x[h] = y[h] = 0.0;
+      if (v[h]) load_coord(P.coords, P.f64, (int64_t)py * P.w1 + px, x[h], y[h]);
+    }
+    const int nv = __popc(__ballot_sync(0xffffffffu, v[0])) + __popc(__ballot_sync(0xffffffffu, v[1]));
+    int mylo_y = 0, myhi_y = 0, mylo_x = 0, myhi_x = 0;  // lane l keeps level l
+    for (int l = 0; l < P.levels; ++l) {
+      int ylo = INT_MAX, yhi = INT_MIN, xlo = INT_MAX, xhi = INT_MIN;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (v[h]) {
+          const LevelPos lp = level_pos(x[h], y[h], l);
+          const int ay = clamp_anchor(lp.y0, r, P.th[l]), ax = clamp_anchor(lp.x0, r, P.tw[l]);
+          ylo = min(ylo, ay);
+          yhi = max(yhi, ay);
+          xlo = min(xlo, ax);
+          xhi = max(xhi, ax);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ylo = min(ylo, __shfl_xor_sync(0xffffffffu, ylo, o));
+        yhi = max(yhi, __shfl_xor_sync(0xffffffffu, yhi, o));
+        xlo = min(xlo, __shfl_xor_sync(0xffffffffu, xlo, o));
+        xhi = max(xhi, __shfl_xor_sync(0xffffffffu, xhi, o));
+      }
+      if (lane == l) {
+        mylo_y = ylo;
+        myhi_y = yhi;
+        mylo_x = xlo;
+        myhi_x = xhi;
+      }
+    }
+    int n_new = 0;
+    unsigned long long c_ovf = 0, c_empty = 0;
+    int* rec = P.plans + tile * PLAN_INTS;
+    if (lane < P.levels) {
+      const int level = lane;
+      const int th = P.th[level], tw = P.tw[level];
+      int32_t* meta = P.meta + (tile * P.levels + level) * CVB_META_INTS;
+      Box B;
+      B.ylo = max(mylo_y - r, 0);
+      B.yhi = min(myhi_y + r + 1, th - 1);
+      B.xlo = max(mylo_x - r, 0);
+      B.xhi = min(myhi_x + r + 1, tw - 1);
+      int status = ST_OK;
+      if (nv == 0 || B.empty()) {
+        status = ST_EMPTY;
+        B = Box{1, 0, 1, 0};
+      } else if (B.h() > P.ch[level] || B.w() > P.cw[level]) {
+        status = ST_OVERFLOW;
+      }
+      const Box prev{meta[0], meta[1], meta[2], meta[3]};
+      const bool prev_ok = !P.no_cache && meta[4] == ST_OK && !prev.empty();
+      const Box I{max(B.ylo, prev.ylo), min(B.yhi, prev.yhi), max(B.xlo, prev.xlo),
+                  min(B.xhi, prev.xhi)};
+      const bool has_i = status == ST_OK && prev_ok && !I.empty();
+      n_new = status == ST_OK ? (int)(B.area() - (has_i ? I.area() : 0)) : 0;
+      meta[0] = B.ylo;
+      meta[1] = B.yhi;
+      meta[2] = B.xlo;
+      meta[3] = B.xhi;
+      meta[4] = status;
+      meta[5] = n_new;
+      const TilePlan tp{B, I, (int)has_i, n_new, nv, status};
+      const int* src = reinterpret_cast<const int*>(&tp);
+      constexpr int TP_INTS = (int)(sizeof(TilePlan) / 4);
+#pragma unroll
+      for (int i = 0; i < TP_INTS; ++i) rec[level * TP_INTS + i] = src[i];
+      c_ovf = status == ST_OVERFLOW;
+      c_empty = status == ST_EMPTY;
+    }
+    // prefix over levels (lane l holds n_new of level l)
+    int pre = n_new;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += u;
+    }
+    int* prefix = rec + CVB_MAX_LEVELS * (int)(sizeof(TilePlan) / 4);
+    if (lane <= P.levels) prefix[lane] = pre - n_new;       // exclusive prefix, lanes 0..L
+    if (lane == P.levels) prefix[CVB_MAX_LEVELS + 1] = pre - n_new;  // n_cells
+    unsigned long long c_dots = (unsigned long long)n_new * nv, c_cells = n_new;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      c_dots += __shfl_xor_sync(0xffffffffu, c_dots, o);
+      c_cells += __shfl_xor_sync(0xffffffffu, c_cells, o);
+      c_ovf += __shfl_xor_sync(0xffffffffu, c_ovf, o);
+      c_empty += __shfl_xor_sync(0xffffffffu, c_empty, o);
+    }
+    if (lane == 0 && P.counters != nullptr) {
+      if (c_dots) atomicAdd(&s_cnt[0], c_dots);
+      if (c_cells) atomicAdd(&s_cnt[1], c_cells);
+      if (c_ovf) atomicAdd(&s_cnt[2], c_ovf);
+      if (c_empty) atomicAdd(&s_cnt[3], c_empty);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 && P.counters != nullptr && s_cnt[threadIdx.x])
+    atomicAdd(P.counters + threadIdx.x, s_cnt[threadIdx.x]);
+}
+
+size_t smem_bytes() {
+  return (size_t)NST * tc::A_STAGE + (size_t)NBP * tc::B_PIECE + sizeof(Ctl) + 1024;
 }
 
 }  // namespace tcp
@@ -843,13 +722,14 @@ size_t smem_bytes(int dp) {
 
 using namespace cvb;
 
+
 extern "C" {
 
 int cvb_tc_sizes(const cvb_partial_desc* desc, int64_t* f1_split_bytes,
                  int64_t* f2_split_bytes_per_level) {
   CVB_REQUIRE(desc, "tc_sizes: null desc");
   CVB_REQUIRE(desc->levels >= 1 && desc->levels <= CVB_MAX_LEVELS, "bad level count");
-  const int dp = (int)ceil_div(desc->d, tc::KS) * tc::KS;
+  const int dp = (int)ceil_div(desc->d, tc::KP) * tc::KP;
   CVB_REQUIRE(dp <= tc::MAX_DP, "tensor-core path supports D <= %d", tc::MAX_DP);
   const int64_t nt = ceil_div(desc->h1, TQH) * ceil_div(desc->w1, TQW);
   if (f1_split_bytes) *f1_split_bytes = nt * 2 * tc::N * dp * 2;
@@ -868,7 +748,7 @@ int cvb_tc_prepare(const cvb_partial_desc* desc, const float* f1,
   CVB_REQUIRE(f1 && f2_levels_host && f1_split && f2_split_host && maxbits,
               "tc_prepare: null pointer");
   cudaStream_t s = as_stream(stream);
-  const int dp = (int)ceil_div(desc->d, tc::KS) * tc::KS;
+  const int dp = (int)ceil_div(desc->d, tc::KP) * tc::KP;
   const int64_t n1 = (int64_t)desc->h1 * desc->w1 * desc->d;
   const int64_t n2 = (int64_t)desc->th[0] * desc->tw[0] * desc->d;
   cudaMemsetAsync(maxbits, 0, 2 * sizeof(uint32_t), s);
@@ -903,7 +783,7 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
   if (st != CVB_OK) return st;
   CVB_REQUIRE(!(flags & CVB_STRICT), "tensor-core contraction has no strict mode");
   CVB_REQUIRE(f1_split && f2_split_host && maxbits, "partial_contract_tc: null pointer");
-  T.dp = (int)ceil_div(desc->d, tc::KS) * tc::KS;
+  T.dp = (int)ceil_div(desc->d, tc::KP) * tc::KP;
   CVB_REQUIRE(T.dp <= tc::MAX_DP, "tensor-core path supports D <= %d", tc::MAX_DP);
   T.f1s = reinterpret_cast<const uint8_t*>(f1_split);
   T.maxbits = maxbits;
@@ -914,39 +794,31 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
     if (used) CVB_REQUIRE(T.f2s[l], "partial_contract_tc: null level pointer");
   }
   if (T.P.ntile == 0) return CVB_OK;
-  static int persistent = -1;
-  if (persistent < 0) {
-    const char* e = getenv("CVB_TC_PERSISTENT");
-    persistent = (e == nullptr || e[0] != '0') ? 1 : 0;
+  static int n_sms = 0;
+  static bool attr = false;
+  static int dbg = -1;
+  if (dbg < 0) {
+    const char* e = getenv("CVB_TC_DEBUG");
+    dbg = e ? atoi(e) : 0;
   }
-  if (persistent) {
-    static int n_sms = 0;
-    static bool attr_p = false;
-    if (n_sms == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const size_t smem = tcp::smem_bytes(T.dp);
-    if (!attr_p) {
-      cudaFuncSetAttribute(tcp::partial_contract_tcp_kernel,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)tcp::smem_bytes(tc::MAX_DP));
-      attr_p = true;
-    }
-    const int64_t grid = T.P.ntile < n_sms ? T.P.ntile : n_sms;
-    tcp::partial_contract_tcp_kernel<<<(unsigned)grid, tcp::THREADS, smem, as_stream(stream)>>>(T);
-    return check_launch("partial_contract_tcp");
+  T.dbg = dbg;
+  if (n_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const size_t smem = (size_t)2 * tc::N * T.dp * 2 + (size_t)tc::NST * tc::A_STAGE;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(tc::partial_contract_tc_kernel,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(tc::MAX_DP * 2 * 2 * tc::N + tc::NST * tc::A_STAGE));
-    attr_set = true;
+  const size_t smem = tcp::smem_bytes();
+  if (!attr) {
+    cudaFuncSetAttribute(tcp::partial_contract_tcp_kernel,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
   }
-  tc::partial_contract_tc_kernel<<<(unsigned)T.P.ntile, tc::THREADS, smem, as_stream(stream)>>>(T);
-  return check_launch("partial_contract_tc");
+  tcp::plan_kernel<<<(unsigned)ceil_div(T.P.ntile, tcp::PLAN_WARPS), tcp::PLAN_WARPS * 32, 0,
+                     as_stream(stream)>>>(T.P);
+  if ((st = check_launch("partial_plan")) != CVB_OK) return st;
+  const int64_t grid = T.P.ntile < n_sms ? T.P.ntile : n_sms;
+  tcp::partial_contract_tcp_kernel<<<(unsigned)grid, tcp::THREADS, smem, as_stream(stream)>>>(T);
+  return check_launch("partial_contract_tcp");
 }
 
 }  // extern "C"

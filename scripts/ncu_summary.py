@@ -39,14 +39,27 @@ for r in raw[2:]:
                 pass
     tot = sum(v for v, _ in items) or 1
     print("   stalls:", ", ".join(f"{n} {100*v/tot:.0f}%" for v, n in sorted(items, reverse=True)[:6]))
-src = list(csv.reader(io.StringIO(run("--page", "source", "--csv"))))
-if len(src) > 2:
-    sh = src[1]
-    ci = {x: i for i, x in enumerate(sh)}
-    data = src[2:]
-    col = "Warp Stall Sampling (All Samples)"
-    tot = sum(float(x[ci[col]] or 0) for x in data) or 1
-    ins = sum(float(x[ci["Instructions Executed"]] or 0) for x in data)
-    print(f"   warp instructions {ins/1e6:.1f}M; top stall lines:")
-    for x in sorted(data, key=lambda x: -float(x[ci[col]] or 0))[:ntop]:
-        print(f"   {100*float(x[ci[col]])/tot:5.1f}% {x[ci['Instructions Executed']]:>9} {x[ci['Source']][:80]}")
+for view in ("sass", "cuda"):
+    text = run("--page", "source", "--csv", "--print-source", view)
+    blocks, cur = [], None
+    for row in csv.reader(io.StringIO(text)):
+        if row and row[0] == "Kernel Name":
+            cur = [row[1], None, []]
+            blocks.append(cur)
+        elif cur is not None and cur[1] is None:
+            cur[1] = row
+        elif cur is not None:
+            cur[2].append(row)
+    for name, sh, data in blocks:
+        if sh is None or not data:
+            continue
+        ci = {x: i for i, x in enumerate(sh)}
+        col = "Warp Stall Sampling (All Samples)"
+        if col not in ci:
+            continue
+        f = lambda x, c: float((x[ci[c]] or "0").replace(",", "")) if x[ci[c]] not in ("-", "") else 0.0
+        tot = sum(f(x, col) for x in data) or 1
+        print(f"== [{view}] {name[:70]}: top stall lines")
+        for x in sorted(data, key=lambda x: -f(x, col))[:ntop]:
+            loc = x[ci["Source"]].strip()[:90]
+            print(f"   {100*f(x, col)/tot:5.1f}% {x[ci['Instructions Executed']]:>9} {loc}")
