@@ -19,6 +19,8 @@
 // as two groups of 4, then per query; tiles whose box overflowed the cache
 // window are evaluated directly (dot products) — all bit-identical in strict
 // mode.
+#include <stdlib.h>
+
 #include "partial.cuh"
 
 namespace cvb {
@@ -430,6 +432,12 @@ static void launch_one(const PartialParams& P, float* out, int l0, int nl, cudaS
 }
 
 int launch_gather_kernel(const PartialParams& P, float* out, bool strict, cudaStream_t s) {
+  static int fast = -1;
+  if (fast < 0) {
+    const char* e = getenv("CVB_GATHER_FAST");
+    fast = (e == nullptr || e[0] != '0') ? 1 : 0;
+  }
+  if (!strict && P.radius == 4 && fast) return launch_gather_fast_r4(P, out, s);
   for (int l0 = 0; l0 < P.levels; l0 += gather::MAXL) {
     const int nl = min(gather::MAXL, P.levels - l0);
     if (P.radius == 4) {

@@ -261,6 +261,8 @@ __device__ __forceinline__ void plan_tile_all_levels(const PartialParams& P, int
 
 // gather/sampler launch (csrc/gather.cu)
 int launch_gather_kernel(const PartialParams& P, float* out, bool strict, cudaStream_t s);
+// fast-arithmetic r=4 sampler (csrc/gather_fast.cu)
+int launch_gather_fast_r4(const PartialParams& P, float* out, cudaStream_t s);
 
 }  // namespace cvb
 

@@ -26,6 +26,7 @@
 //     removes the power-of-two scales and writes each cell's 64 query costs
 //     into its cache slot.
 #include <cuda_fp16.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "partial.cuh"
@@ -186,6 +187,7 @@ struct TcParams {
   const uint32_t* maxbits;             // [0] max|F1|, [1] max|F2|
   int dp;
   int dbg;                             // profiling knockouts (CVB_TC_DEBUG), 0 in production
+  unsigned long long* ts;              // role timeline (CVB_TC_DEBUG & 16), null in production
 };
 
 __global__ void absmax_kernel(const float* __restrict__ x, int64_t n, uint32_t* out) {
@@ -333,6 +335,14 @@ __device__ __forceinline__ void arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+__device__ __forceinline__ void stamp(const tc::TcParams& T, int64_t it, int e) {
+  if (T.ts != nullptr && blockIdx.x < 4 && it < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    T.ts[((int64_t)blockIdx.x * 64 + it) * 8 + e] = t;
+  }
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     partial_contract_tcp_kernel(const __grid_constant__ tc::TcParams T) {
   extern __shared__ uint8_t smem_raw[];
@@ -402,6 +412,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                          U(C.b_full[bs]));
           }
         }
+        stamp(T, it, 5);
         arrive(U(C.plan_empty[s]));
       }
     }
@@ -414,6 +425,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (t >= P.ntile) break;
         const int s = (int)(it % NPL);
         wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
+        stamp(T, it, 1);
         const int n = C.slot[s].n_cells;
         if (n > 0) {
           const int n_chunks = (n + tc::M - 1) / tc::M;
@@ -451,6 +463,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           pb += n_kb;
         }
+        stamp(T, it, 2);
         arrive(U(C.plan_empty[s]));
       }
     }
@@ -465,6 +478,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::mbar_expect_tx(U(C.plan_full[s]), (uint32_t)sizeof(PlanRec));
         tc::bulk_g2s(tc::smem_u32(&C.slot[s]), P.plans + (P.tile0 + t) * PLAN_INTS,
                      (uint32_t)sizeof(PlanRec), U(C.plan_full[s]));
+        stamp(T, it, 0);
       }
     }
   } else if (warp >= 4 && warp < 8) {
@@ -522,6 +536,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
+      if (tid == 128) stamp(T, it, 3);
       arrive(U(C.plan_empty[s]));
     }
   } else if (warp >= 8) {
@@ -576,6 +591,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::tc_fence_before();
         arrive(U(C.acc_empty[ab]));
       }
+      if (tid == 256) stamp(T, it, 4);
       arrive(U(C.plan_empty[s]));
     }
   }
@@ -802,6 +818,13 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
     dbg = e ? atoi(e) : 0;
   }
   T.dbg = dbg;
+  static unsigned long long* ts_buf = nullptr;
+  T.ts = nullptr;
+  if (dbg & 16) {
+    if (ts_buf == nullptr) cudaMalloc(&ts_buf, 4 * 64 * 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(ts_buf, 0, 4 * 64 * 8 * sizeof(unsigned long long), as_stream(stream));
+    T.ts = ts_buf;
+  }
   if (n_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -818,6 +841,22 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
   if ((st = check_launch("partial_plan")) != CVB_OK) return st;
   const int64_t grid = T.P.ntile < n_sms ? T.P.ntile : n_sms;
   tcp::partial_contract_tcp_kernel<<<(unsigned)grid, tcp::THREADS, smem, as_stream(stream)>>>(T);
+  if (T.ts != nullptr) {  // debug timeline dump (CTA 0..3, first 64 tiles each), ns
+    unsigned long long h[4 * 64 * 8];
+    cudaStreamSynchronize(as_stream(stream));
+    cudaMemcpy(h, T.ts, sizeof(h), cudaMemcpyDeviceToHost);
+    static int call = 0;
+    ++call;
+    const unsigned long long t0 = h[0];
+    for (int b = 0; b < 2; ++b)
+      for (int it = 0; it < 64; ++it) {
+        const unsigned long long* e = h + (b * 64 + it) * 8;
+        if (e[1] == 0) break;
+        fprintf(stderr, "TS call %d cta %d it %2d plan %7.2f mma0 %7.2f mma1 %7.2f A %7.2f epi %7.2f B %7.2f\n",
+                call, b, it, (e[0] - t0) * 1e-3, (e[1] - t0) * 1e-3, (e[2] - t0) * 1e-3,
+                (e[3] - t0) * 1e-3, (e[4] - t0) * 1e-3, (e[5] - t0) * 1e-3);
+      }
+  }
   return check_launch("partial_contract_tcp");
 }
 
