@@ -52,6 +52,7 @@ typedef enum {
 #define CVB_STRICT 1          /* reference-exact arithmetic                 */
 #define CVB_COORDS_F64 2      /* centroid field is float64 (else float32)   */
 #define CVB_NO_CACHE 4        /* partial sampler: recompute every iteration */
+#define CVB_PREP_POOL 8       /* cvb_tc_prepare: also build pyramid levels >= 1 */
 
 #define CVB_MAX_LEVELS 8
 
@@ -192,20 +193,22 @@ int cvb_partial_gather(const cvb_partial_desc* desc, const float* f1,
 /* Tensor-core contraction (fast path, D <= 256): the same tiler, metadata
  * and cache as cvb_partial_contract, with the new-cell contraction on
  * tcgen05 (kind::f16, split-fp16 operands, 3 MMAs per K-step, fp32
- * accumulation in TMEM).  cvb_tc_prepare splits F1 (per-tile images) and the
- * fmap2 pyramid (hi/lo planes) once per image pair; maxbits is device
- * workspace (2 x uint32).  Not bit-exact: use cvb_partial_contract with
- * CVB_STRICT for reference-exact arithmetic. */
+ * accumulation in TMEM).  cvb_tc_prepare splits F1 (per-tile B-operand
+ * images) and every pyramid level (hi/lo planes) once per image pair, each
+ * row scaled by its own power of two (stored as an exponent byte after the
+ * planes); with CVB_PREP_POOL it also produces pyramid levels >= 1 from
+ * level 0 (the reference's pool2x2, bit-exact, dense.py:71-86) in the same
+ * pass, so f2_levels_host[1..] are outputs.  Not bit-exact in the dots: use
+ * cvb_partial_contract with CVB_STRICT for reference-exact arithmetic. */
 int cvb_tc_sizes(const cvb_partial_desc* desc, int64_t* f1_split_bytes,
                  int64_t* f2_split_bytes_per_level);
-int cvb_tc_prepare(const cvb_partial_desc* desc, const float* f1,
-                   const float* const* f2_levels_host, void* f1_split,
-                   void* const* f2_split_host, uint32_t* maxbits, void* stream);
+int cvb_tc_prepare(const cvb_partial_desc* desc, const float* f1, float* const* f2_levels_host,
+                   void* f1_split, void* const* f2_split_host, int32_t flags, void* stream);
 int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
                             const float* const* f2_levels_host, const void* f1_split,
-                            const void* const* f2_split_host, const uint32_t* maxbits,
-                            const void* coords, int32_t* meta, float* const* cache_levels_host,
-                            unsigned long long* counters, int32_t flags, void* stream);
+                            const void* const* f2_split_host, const void* coords, int32_t* meta,
+                            float* const* cache_levels_host, unsigned long long* counters,
+                            int32_t flags, void* stream);
 
 /* ---- reference block-sparse state (sparse.py:262-309) ------------------- */
 

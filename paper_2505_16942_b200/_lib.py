@@ -26,6 +26,7 @@ CVB_ERR_CUDA = 4
 CVB_STRICT = 1
 CVB_COORDS_F64 = 2
 CVB_NO_CACHE = 4
+CVB_PREP_POOL = 8
 
 MAX_LEVELS = 8
 TILE_H = 8
@@ -78,11 +79,10 @@ SIGNATURES = {
     "cvb_partial_gather": (C.c_int, [C.POINTER(PartialDesc), _p, C.POINTER(_p), _p, _f32, _p,
                                      C.POINTER(_p), _p, _i32, _p]),
     "cvb_tc_sizes": (C.c_int, [C.POINTER(PartialDesc), C.POINTER(_i64), C.POINTER(_i64)]),
-    "cvb_tc_prepare": (C.c_int, [C.POINTER(PartialDesc), _p, C.POINTER(_p), _p, C.POINTER(_p), _p,
-                                 _p]),
+    "cvb_tc_prepare": (C.c_int, [C.POINTER(PartialDesc), _p, C.POINTER(_p), _p, C.POINTER(_p),
+                                 _i32, _p]),
     "cvb_partial_contract_tc": (C.c_int, [C.POINTER(PartialDesc), _p, C.POINTER(_p), _p,
-                                          C.POINTER(_p), _p, _p, _p, C.POINTER(_p), _p, _i32,
-                                          _p]),
+                                          C.POINTER(_p), _p, _p, C.POINTER(_p), _p, _i32, _p]),
     "cvb_computation_mask": (C.c_int, [_p, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _p,
                                        _i64, _p]),
     "cvb_block_indices_workspace": (_i64, [_i64]),

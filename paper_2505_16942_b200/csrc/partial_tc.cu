@@ -134,6 +134,9 @@ __device__ __forceinline__ void cp_async_wait() {
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -157,15 +160,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// power-of-two exponent e with max * 2^e < 2^TARGET_EXP (0 for an all-zero tensor)
-__device__ __forceinline__ int scale_exp(uint32_t maxbits) {
-  const float m = __uint_as_float(maxbits);
+// power-of-two exponent e with m * 2^e < 2^TARGET_EXP (0 for an all-zero row)
+__device__ __forceinline__ int scale_exp(float m) {
   if (!(m > 0.f) || !isfinite(m)) return 0;
   int k;
   frexpf(m, &k);  // m < 2^k
-  int e = TARGET_EXP - k;
+  const int e = TARGET_EXP - k;
   return e < -60 ? -60 : (e > 60 ? 60 : e);
 }
+
+// 2^-e as a float (|e| <= 60)
+__device__ __forceinline__ float exp2_neg(int e) { return __int_as_float((127 - e) << 23); }
 
 __device__ __forceinline__ void split8(const float (&x)[8], float s, uint4& hi, uint4& lo) {
   __half h[8], l[8];
@@ -181,76 +186,123 @@ __device__ __forceinline__ void split8(const float (&x)[8], float s, uint4& hi, 
 
 struct TcParams {
   PartialParams P;
-  const uint8_t* f1s;                  // [tiles][2][8 rg][dp/8 kg][8][8] fp16
+  const uint8_t* f1s;                  // per tile: [dp/KP pieces][hi, lo][8 rg][KP/8 kg][8][8] fp16
+  const int8_t* e1;                    // per tile: 64 query exponents
   const __half* f2s[CVB_MAX_LEVELS];   // hi plane [th*tw][dp]; lo = hi + plane
+  const int8_t* e2[CVB_MAX_LEVELS];    // per cell exponent
   int64_t plane[CVB_MAX_LEVELS];
-  const uint32_t* maxbits;             // [0] max|F1|, [1] max|F2|
   int dp;
   int dbg;                             // profiling knockouts (CVB_TC_DEBUG), 0 in production
   unsigned long long* ts;              // role timeline (CVB_TC_DEBUG & 16), null in production
 };
 
-__global__ void absmax_kernel(const float* __restrict__ x, int64_t n, uint32_t* out) {
-  float m = 0.f;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    m = fmaxf(m, fabsf(__ldg(x + i)));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
-}
+// Operand preparation, once per image pair.  Every row (a query of F1, a
+// cell of a pyramid level) gets its own power-of-two exponent e (max|x| 2^e
+// < 2^14, so hi and lo stay normal fp16) and is split into hi/lo fp16; the
+// epilogue removes 2^-(e_q + e_c) exactly.  One warp per row, lane = 8
+// channels.
 
-// F1 -> per-tile image of the B operand, cut into K pieces of KP channels:
-// [dp/KP pieces][hi, lo][8 row groups][KP/8 k groups][8 rows][8 channels] fp16
-__global__ void split_f1_kernel(const float* __restrict__ f1, int h1, int w1, int d, int dp,
-                                int tiles_x, int64_t n_tiles, const uint32_t* maxbits,
-                                uint8_t* __restrict__ out) {
-  const int kgs = dp / 8;
-  const int64_t total = n_tiles * N * kgs;
-  const float s = ldexpf(1.f, scale_exp(maxbits[0]));
-  const int64_t tile_bytes = (int64_t)N * dp * 2 * 2;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int kg = (int)(i % kgs);
-    const int q = (int)((i / kgs) % N);
-    const int64_t tile = i / ((int64_t)kgs * N);
-    const int py = (int)(tile / tiles_x) * TQH + q / TQW, px = (int)(tile % tiles_x) * TQW + q % TQW;
-    float x[8];
+__device__ __forceinline__ void load8(const float* __restrict__ row, int d, int kg, bool vec,
+                                      float (&x)[8]) {
+  if (vec && kg * 8 + 8 <= d) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(row + kg * 8));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(row + kg * 8 + 4));
+    x[0] = a.x, x[1] = a.y, x[2] = a.z, x[3] = a.w, x[4] = b.x, x[5] = b.y, x[6] = b.z, x[7] = b.w;
+  } else {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int k = kg * 8 + j;
-      x[j] = (py < h1 && px < w1 && k < d) ? __ldg(f1 + ((int64_t)py * w1 + px) * d + k) : 0.f;
-    }
-    uint4 hi, lo;
-    split8(x, s, hi, lo);
-    const int piece = kg / (KP / 8), kgi = kg % (KP / 8);
-    uint8_t* base = out + tile * tile_bytes + (int64_t)piece * B_PIECE + (q / 8) * (KP / 8 * 128) +
-                    kgi * 128 + (q % 8) * 16;
-    *reinterpret_cast<uint4*>(base) = hi;
-    *reinterpret_cast<uint4*>(base + B_HALF) = lo;
+    for (int j = 0; j < 8; ++j) x[j] = kg * 8 + j < d ? __ldg(row + kg * 8 + j) : 0.f;
   }
 }
 
-// F2 level -> hi/lo planes [cells][dp] fp16
-__global__ void split_f2_kernel(const float* __restrict__ f2, int64_t cells, int d, int dp,
-                                const uint32_t* maxbits, __half* __restrict__ out) {
-  const int kgs = dp / 8;
-  const int64_t total = cells * kgs;
-  const float s = ldexpf(1.f, scale_exp(maxbits[1]));
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int kg = (int)(i % kgs);
-    const int64_t c = i / kgs;
-    float x[8];
+__device__ __forceinline__ int row_exp(const float (&x)[8]) {
+  float m = 0.f;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int k = kg * 8 + j;
-      x[j] = k < d ? __ldg(f2 + c * d + k) : 0.f;
+  for (int j = 0; j < 8; ++j) m = fmaxf(m, fabsf(x[j]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  return scale_exp(m);
+}
+
+// F1 -> per-tile B-operand images + query exponents
+__global__ void __launch_bounds__(256) split_f1_kernel(const float* __restrict__ f1, int h1,
+                                                       int w1, int d, int dp, int tiles_x,
+                                                       int64_t n_tiles, bool vec,
+                                                       uint8_t* __restrict__ out,
+                                                       int8_t* __restrict__ exps) {
+  const int lane = threadIdx.x & 31, kgs = dp / 8;
+  const int64_t tile_bytes = (int64_t)N * dp * 2 * 2;
+  const int64_t rows = n_tiles * N;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int q = (int)(r % N);
+    const int64_t tile = r / N;
+    const int py = (int)(tile / tiles_x) * TQH + q / TQW, px = (int)(tile % tiles_x) * TQW + q % TQW;
+    float x[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (lane < kgs && py < h1 && px < w1) load8(f1 + ((int64_t)py * w1 + px) * d, d, lane, vec, x);
+    const int e = row_exp(x);
+    if (lane < kgs) {
+      uint4 hi, lo;
+      split8(x, exp2_neg(-e), hi, lo);
+      const int piece = lane / (KP / 8), kgi = lane % (KP / 8);
+      uint8_t* base = out + tile * tile_bytes + (int64_t)piece * B_PIECE +
+                      (q / 8) * (KP / 8 * 128) + kgi * 128 + (q % 8) * 16;
+      *reinterpret_cast<uint4*>(base) = hi;
+      *reinterpret_cast<uint4*>(base + B_HALF) = lo;
     }
-    uint4 hi, lo;
-    split8(x, s, hi, lo);
-    *reinterpret_cast<uint4*>(out + c * dp + kg * 8) = hi;
-    *reinterpret_cast<uint4*>(out + cells * dp + c * dp + kg * 8) = lo;
+    if (lane == 0) exps[r] = (int8_t)e;
+  }
+}
+
+// One pyramid level -> hi/lo planes [cells][dp] + cell exponents.  With
+// `pool`, the level is first produced from the previous one by the
+// reference's 2x2 average pool (((a+b)+(c+d))*0.25, bit-exact with
+// pool2x2_vec4_kernel) and also written out in fp32.
+__device__ __forceinline__ float pool4f(float a, float b, float c, float d) {
+  return __fmul_rn(__fadd_rn(__fadd_rn(a, b), __fadd_rn(c, d)), 0.25f);
+}
+
+__global__ void __launch_bounds__(256) split_level_kernel(const float* __restrict__ src,
+                                                          int src_w, float* __restrict__ pooled,
+                                                          int h, int w, int d, int dp, bool pool,
+                                                          bool vec, __half* __restrict__ planes,
+                                                          int8_t* __restrict__ exps) {
+  const int lane = threadIdx.x & 31, kgs = dp / 8;
+  const int64_t cells = (int64_t)h * w;
+  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < cells;
+       c += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    float x[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (lane < kgs) {
+      if (pool) {
+        const int y = (int)(c / w), xx = (int)(c % w);
+        const float* r0 = src + ((int64_t)(2 * y) * src_w + 2 * xx) * d;
+        const float* r1 = r0 + (int64_t)src_w * d;
+        float a[8], b[8], e[8], f[8];
+        load8(r0, d, lane, vec, a);
+        load8(r0 + d, d, lane, vec, b);
+        load8(r1, d, lane, vec, e);
+        load8(r1 + d, d, lane, vec, f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = pool4f(a[j], b[j], e[j], f[j]);
+        float* o = pooled + c * d;
+        if (vec && lane * 8 + 8 <= d) {
+          *reinterpret_cast<float4*>(o + lane * 8) = make_float4(x[0], x[1], x[2], x[3]);
+          *reinterpret_cast<float4*>(o + lane * 8 + 4) = make_float4(x[4], x[5], x[6], x[7]);
+        } else {
+          for (int j = 0; j < 8; ++j)
+            if (lane * 8 + j < d) o[lane * 8 + j] = x[j];
+        }
+      } else {
+        load8(src + c * d, d, lane, vec, x);
+      }
+    }
+    const int e = row_exp(x);
+    if (lane < kgs) {
+      uint4 hi, lo;
+      split8(x, exp2_neg(-e), hi, lo);
+      *reinterpret_cast<uint4*>(planes + c * dp + lane * 8) = hi;
+      *reinterpret_cast<uint4*>(planes + cells * dp + c * dp + lane * 8) = lo;
+    }
+    if (lane == 0) exps[c] = (int8_t)e;
   }
 }
 
@@ -306,6 +358,7 @@ struct Ctl {
   uint64_t a_full[NST], a_empty[NST];
   uint64_t acc_full[2], acc_empty[2];
   PlanRec slot[NPL];
+  float qscale[tc::N];
   uint32_t tmem;
 };
 
@@ -543,9 +596,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------- epilogue (128 threads = TMEM lanes) ----------------
     const int ep = tid - 256;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const float s_main =
-        ldexpf(1.f, -(tc::scale_exp(T.maxbits[0]) + tc::scale_exp(T.maxbits[1])));
-    const float s_corr = s_main * (1.f / (float)(1 << tc::LOG2_LO));
+    float* s_q = reinterpret_cast<float*>(&C.qscale[0]);
     uint32_t cg = 0;
     for (int64_t it = 0;; ++it) {
       const int64_t t = blockIdx.x + it * gridDim.x;
@@ -556,6 +607,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       const PlanRec& S = C.slot[s];
       const int n = S.n_cells;
       const int n_chunks = (n + tc::M - 1) / tc::M;
+      if (n_chunks > 0) {
+        // the tile's 64 query scales 2^-e_q
+        tc::named_bar(1, 128);
+        if (ep < tc::N) s_q[ep] = tc::exp2_neg(T.e1[tile * tc::N + ep]);
+        tc::named_bar(1, 128);
+      }
       for (int c = 0; c < n_chunks; ++c, ++cg) {
         const int ab = cg & 1;
         wait_full(U(C.acc_full[ab]), cg >> 1);
@@ -563,12 +620,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int gi = c * tc::M + ep;
         float* dst = nullptr;
         int64_t plane = 0;
+        float s_c = 0.f;
         if (gi < n) {
           const tc::CellRef cr = tc::cell_of(gi, S.plan, S.prefix, P.levels);
           const int ch = P.ch[cr.level], cw = P.cw[cr.level];
           plane = (int64_t)ch * cw * TQW;
           dst = P.cache[cr.level] + tile * plane * TQH +
                 (int64_t)slot_of(cr.cy, cr.cx, ch, cw) * TQW;
+          s_c = tc::exp2_neg(T.e2[cr.level][(int64_t)cr.cy * P.tw[cr.level] + cr.cx]);
         }
         float vm[32], vc[32];
 #pragma unroll
@@ -578,12 +637,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (dst != nullptr && !(T.dbg & 2)) {
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
-              float4 o;
-              o.x = fmaf(vc[j + 0], s_corr, vm[j + 0] * s_main);
-              o.y = fmaf(vc[j + 1], s_corr, vm[j + 1] * s_main);
-              o.z = fmaf(vc[j + 2], s_corr, vm[j + 2] * s_main);
-              o.w = fmaf(vc[j + 3], s_corr, vm[j + 3] * s_main);
               const int q = h * 32 + j;
+              float4 o;
+              // (main + 2^-11 corr) * 2^-(e_q + e_c): exact power-of-two scales
+              o.x = fmaf(vc[j + 0], 1.f / (1 << tc::LOG2_LO), vm[j + 0]) * (s_q[q + 0] * s_c);
+              o.y = fmaf(vc[j + 1], 1.f / (1 << tc::LOG2_LO), vm[j + 1]) * (s_q[q + 1] * s_c);
+              o.z = fmaf(vc[j + 2], 1.f / (1 << tc::LOG2_LO), vm[j + 2]) * (s_q[q + 2] * s_c);
+              o.w = fmaf(vc[j + 3], 1.f / (1 << tc::LOG2_LO), vm[j + 3]) * (s_q[q + 3] * s_c);
               *reinterpret_cast<float4*>(dst + (q >> 3) * plane + (q & 7)) = o;
             }
           }
@@ -748,65 +808,81 @@ int cvb_tc_sizes(const cvb_partial_desc* desc, int64_t* f1_split_bytes,
   const int dp = (int)ceil_div(desc->d, tc::KP) * tc::KP;
   CVB_REQUIRE(dp <= tc::MAX_DP, "tensor-core path supports D <= %d", tc::MAX_DP);
   const int64_t nt = ceil_div(desc->h1, TQH) * ceil_div(desc->w1, TQW);
-  if (f1_split_bytes) *f1_split_bytes = nt * 2 * tc::N * dp * 2;
+  // F1: per-tile B images, then one exponent byte per query
+  if (f1_split_bytes) *f1_split_bytes = nt * tc::N * dp * 4 + nt * tc::N;
+  // per level: hi plane, lo plane, then one exponent byte per cell
   if (f2_split_bytes_per_level)
-    for (int l = 0; l < desc->levels; ++l)
-      f2_split_bytes_per_level[l] = 2 * (int64_t)desc->th[l] * desc->tw[l] * dp * 2;
+    for (int l = 0; l < desc->levels; ++l) {
+      const int64_t cells = (int64_t)desc->th[l] * desc->tw[l];
+      f2_split_bytes_per_level[l] = 4 * cells * dp + ceil_div(cells, 16) * 16;
+    }
   return CVB_OK;
 }
 
-int cvb_tc_prepare(const cvb_partial_desc* desc, const float* f1,
-                   const float* const* f2_levels_host, void* f1_split,
-                   void* const* f2_split_host, uint32_t* maxbits, void* stream) {
+static int prep_grid(int64_t rows) {
+  const int64_t g = ceil_div(rows, 8);
+  return (int)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
+}
+
+int cvb_tc_prepare(const cvb_partial_desc* desc, const float* f1, float* const* f2_levels_host,
+                   void* f1_split, void* const* f2_split_host, int32_t flags, void* stream) {
   int64_t f1b = 0;
   int st = cvb_tc_sizes(desc, &f1b, nullptr);
   if (st != CVB_OK) return st;
-  CVB_REQUIRE(f1 && f2_levels_host && f1_split && f2_split_host && maxbits,
-              "tc_prepare: null pointer");
+  CVB_REQUIRE(f1 && f2_levels_host && f1_split && f2_split_host, "tc_prepare: null pointer");
   cudaStream_t s = as_stream(stream);
-  const int dp = (int)ceil_div(desc->d, tc::KP) * tc::KP;
-  const int64_t n1 = (int64_t)desc->h1 * desc->w1 * desc->d;
-  const int64_t n2 = (int64_t)desc->th[0] * desc->tw[0] * desc->d;
-  cudaMemsetAsync(maxbits, 0, 2 * sizeof(uint32_t), s);
-  tc::absmax_kernel<<<148 * 4, 256, 0, s>>>(f1, n1, maxbits);
-  if ((st = check_launch("tc_absmax")) != CVB_OK) return st;
-  tc::absmax_kernel<<<148 * 4, 256, 0, s>>>(f2_levels_host[0], n2, maxbits + 1);
-  if ((st = check_launch("tc_absmax")) != CVB_OK) return st;
+  const int d = desc->d;
+  const int dp = (int)ceil_div(d, tc::KP) * tc::KP;
   const int tiles_x = (int)ceil_div(desc->w1, TQW);
   const int64_t n_tiles = ceil_div(desc->h1, TQH) * tiles_x;
-  tc::split_f1_kernel<<<148 * 8, 256, 0, s>>>(f1, desc->h1, desc->w1, desc->d, dp, tiles_x,
-                                              n_tiles, maxbits,
-                                              reinterpret_cast<uint8_t*>(f1_split));
+  bool vec = d % 4 == 0 && ((uintptr_t)f1 & 15) == 0;
+  uint8_t* f1s = reinterpret_cast<uint8_t*>(f1_split);
+  tc::split_f1_kernel<<<prep_grid(n_tiles * tc::N), 256, 0, s>>>(
+      f1, desc->h1, desc->w1, d, dp, tiles_x, n_tiles, vec, f1s,
+      reinterpret_cast<int8_t*>(f1s + n_tiles * tc::N * dp * 4));
   if ((st = check_launch("tc_split_f1")) != CVB_OK) return st;
+  const bool pool = flags & CVB_PREP_POOL;
   for (int l = 0; l < desc->levels; ++l) {
     CVB_REQUIRE(f2_levels_host[l] && f2_split_host[l], "tc_prepare: null level pointer");
-    tc::split_f2_kernel<<<148 * 8, 256, 0, s>>>(
-        f2_levels_host[l], (int64_t)desc->th[l] * desc->tw[l], desc->d, dp, maxbits,
-        reinterpret_cast<__half*>(f2_split_host[l]));
-    if ((st = check_launch("tc_split_f2")) != CVB_OK) return st;
+    const int h = desc->th[l], w = desc->tw[l];
+    const int64_t cells = (int64_t)h * w;
+    const bool pool_l = pool && l > 0;
+    if (pool_l)
+      CVB_REQUIRE(desc->th[l - 1] / 2 == h && desc->tw[l - 1] / 2 == w,
+                  "tc_prepare: level %d dims are not the 2x2 pool of level %d", l, l - 1);
+    const float* src = pool_l ? f2_levels_host[l - 1] : f2_levels_host[l];
+    const bool v = d % 4 == 0 && ((uintptr_t)src & 15) == 0 &&
+                   ((uintptr_t)f2_levels_host[l] & 15) == 0;
+    __half* planes = reinterpret_cast<__half*>(f2_split_host[l]);
+    tc::split_level_kernel<<<prep_grid(cells), 256, 0, s>>>(
+        src, pool_l ? desc->tw[l - 1] : w, f2_levels_host[l], h, w, d, dp, pool_l, v, planes,
+        reinterpret_cast<int8_t*>(planes + 2 * cells * dp));
+    if ((st = check_launch("tc_split_level")) != CVB_OK) return st;
   }
   return CVB_OK;
 }
 
 int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
                             const float* const* f2_levels_host, const void* f1_split,
-                            const void* const* f2_split_host, const uint32_t* maxbits,
-                            const void* coords, int32_t* meta, float* const* cache_levels_host,
-                            unsigned long long* counters, int32_t flags, void* stream) {
+                            const void* const* f2_split_host, const void* coords, int32_t* meta,
+                            float* const* cache_levels_host, unsigned long long* counters,
+                            int32_t flags, void* stream) {
   tc::TcParams T;
   int st = cvb_internal_build_params(desc, f1, f2_levels_host, coords, 1.0f, meta,
                                      cache_levels_host, counters, flags, T.P);
   if (st != CVB_OK) return st;
   CVB_REQUIRE(!(flags & CVB_STRICT), "tensor-core contraction has no strict mode");
-  CVB_REQUIRE(f1_split && f2_split_host && maxbits, "partial_contract_tc: null pointer");
+  CVB_REQUIRE(f1_split && f2_split_host, "partial_contract_tc: null pointer");
   T.dp = (int)ceil_div(desc->d, tc::KP) * tc::KP;
   CVB_REQUIRE(T.dp <= tc::MAX_DP, "tensor-core path supports D <= %d", tc::MAX_DP);
   T.f1s = reinterpret_cast<const uint8_t*>(f1_split);
-  T.maxbits = maxbits;
+  const int64_t n_tiles_all = T.P.n_tiles;
+  T.e1 = reinterpret_cast<const int8_t*>(T.f1s + n_tiles_all * tc::N * T.dp * 4);
   for (int l = 0; l < CVB_MAX_LEVELS; ++l) {
     const bool used = l < desc->levels;
     T.f2s[l] = used ? reinterpret_cast<const __half*>(f2_split_host[l]) : nullptr;
     T.plane[l] = used ? (int64_t)desc->th[l] * desc->tw[l] * T.dp : 0;
+    T.e2[l] = used ? reinterpret_cast<const int8_t*>(T.f2s[l] + 2 * T.plane[l]) : nullptr;
     if (used) CVB_REQUIRE(T.f2s[l], "partial_contract_tc: null level pointer");
   }
   if (T.P.ntile == 0) return CVB_OK;

@@ -29,8 +29,9 @@ def pooled_dims(shape: Tuple[int, int], level: int) -> Tuple[int, int]:
     return h, w
 
 
-def build_feature_pyramid(f2: FeatureMap, levels: int) -> FeaturePyramid:
-    """L-level pyramid of f2 (dense.py:71-86)."""
+def alloc_feature_pyramid(f2: FeatureMap, levels: int) -> FeaturePyramid:
+    """Pyramid storage for f2 with levels >= 1 allocated but not yet pooled
+    (validation as dense.py:71-86); a fused producer fills them."""
     if levels < 1:
         raise ValueError("levels must be >= 1")
     fh, fw = pooled_dims((f2.height, f2.width), levels - 1)
@@ -38,14 +39,21 @@ def build_feature_pyramid(f2: FeatureMap, levels: int) -> FeaturePyramid:
         raise ValueError(
             f"pyramid of {levels} levels on {f2.height}x{f2.width} would produce an empty level")
     require_cuda(f2.values)
-    outs = [f2.values]
+    maps = [f2]
     for lvl in range(1, levels):
         h, w = pooled_dims((f2.height, f2.width), lvl)
-        outs.append(torch.empty((h, w, f2.dims), dtype=torch.float32, device=f2.values.device))
+        maps.append(FeatureMap(values=torch.empty((h, w, f2.dims), dtype=torch.float32,
+                                                  device=f2.values.device), check=False))
+    return FeaturePyramid(levels=maps)
+
+
+def build_feature_pyramid(f2: FeatureMap, levels: int) -> FeaturePyramid:
+    """L-level pyramid of f2 (dense.py:71-86)."""
+    pyr = alloc_feature_pyramid(f2, levels)
+    outs = [m.values for m in pyr.levels]
     _lib.call("cvb_build_pyramid", _lib.ptr(f2.values), f2.height, f2.width, f2.dims, levels,
               _lib.ptr_array(outs), stream_handle())
-    maps = [f2] + [FeatureMap(values=o, check=False) for o in outs[1:]]
-    return FeaturePyramid(levels=maps)
+    return pyr
 
 
 def build_dense_volume(f1: FeatureMap, f2: FeatureMap, backend: Optional[str] = None,

@@ -31,7 +31,7 @@ import torch
 
 from . import _lib
 from ._backend import resolve_backend, stream_handle
-from .dense import build_feature_pyramid, coords_flags, pooled_dims
+from .dense import alloc_feature_pyramid, build_feature_pyramid, coords_flags, pooled_dims
 from .types import (CacheLimitError, CentroidField, CostMaps, FeatureMap, FeaturePyramid,
                     GatherMissError, LookupSpec, WorkCounter, require_cuda)
 
@@ -259,7 +259,6 @@ class SparseVolumeState:
         self.n_tiles = 0
         self.tc_f1 = None
         self.tc_f2 = None
-        self.tc_max = None
 
     # -- reference-compatible attributes ------------------------------------
     @property
@@ -335,7 +334,18 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
     if mode not in MODES:
         raise ValueError(f"mode must be one of {MODES}, got {mode!r}")
     require_cuda(f1.values, f2.values)
-    pyr = pyramid if pyramid is not None else build_feature_pyramid(f2, spec.levels)
+    if tensor_cores is None:
+        tensor_cores = mode == "tile" and (not strict) and f1.dims <= 256
+    if tensor_cores and strict:
+        raise ValueError("strict arithmetic runs on the FP32 pipe; tensor_cores=False")
+    # on the tensor-core path the operand split builds the pyramid in the same pass
+    fuse_pyramid = tensor_cores and mode == "tile" and pyramid is None
+    if pyramid is not None:
+        pyr = pyramid
+    elif fuse_pyramid:
+        pyr = alloc_feature_pyramid(f2, spec.levels)
+    else:
+        pyr = build_feature_pyramid(f2, spec.levels)
     if len(pyr) < spec.levels:
         raise ValueError("pyramid has fewer levels than the spec")
     pm1 = PaddedGrid.of(f1.height, f1.width, f1.dims, block)
@@ -374,12 +384,8 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
             lv.cache = torch.empty(per_level[lvl], dtype=torch.float32, device=dev)
         _lib.call("cvb_partial_reset", _lib.C.byref(desc), _lib.ptr(state.meta),
                   stream_handle())
-        if tensor_cores is None:
-            tensor_cores = (not strict) and f1.dims <= 256
         if tensor_cores:
-            if strict:
-                raise ValueError("strict arithmetic runs on the FP32 pipe; tensor_cores=False")
-            _prepare_tc(state)
+            _prepare_tc(state, pool=fuse_pyramid)
             # overlap contraction and gathering across tile ranges when the frame
             # spans many waves (>= 8 tiles per SM)
             if pipeline_splits is None:
@@ -399,8 +405,10 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
     return state
 
 
-def _prepare_tc(state: SparseVolumeState) -> None:
-    """Split F1 / the fmap2 pyramid into fp16 hi/lo operands (once per pair)."""
+def _prepare_tc(state: SparseVolumeState, pool: bool = False) -> None:
+    """Split F1 / the fmap2 pyramid into per-row-scaled fp16 hi/lo operands
+    (once per pair); with `pool`, pyramid levels >= 1 are produced in the
+    same pass (bit-exact pool2x2)."""
     spec = state.spec
     f1b = _lib.C.c_int64()
     per = (_lib.C.c_int64 * _lib.MAX_LEVELS)()
@@ -409,11 +417,10 @@ def _prepare_tc(state: SparseVolumeState) -> None:
     state.tc_f1 = torch.empty(f1b.value, dtype=torch.uint8, device=dev)
     state.tc_f2 = [torch.empty(per[l], dtype=torch.uint8, device=dev)
                    for l in range(spec.levels)]
-    state.tc_max = torch.zeros(2, dtype=torch.int32, device=dev)
     f2s = [state.pyramid.levels[l].values for l in range(spec.levels)]
     _lib.call("cvb_tc_prepare", _lib.C.byref(state.desc), _lib.ptr(state.f1.values),
               _lib.ptr_array(f2s), _lib.ptr(state.tc_f1), _lib.ptr_array(state.tc_f2),
-              _lib.ptr(state.tc_max), stream_handle())
+              _lib.CVB_PREP_POOL if pool else 0, stream_handle())
     state.tc = True
 
 
@@ -429,7 +436,7 @@ def _contract(state: SparseVolumeState, centroids: CentroidField, flags: int, f2
     if state.tc:
         _lib.call("cvb_partial_contract_tc", _lib.C.byref(state.desc), _lib.ptr(state.f1.values),
                   f2s, _lib.ptr(state.tc_f1), _lib.ptr_array(state.tc_f2),
-                  _lib.ptr(state.tc_max), _lib.ptr(centroids.coords), _lib.ptr(state.meta),
+                  _lib.ptr(centroids.coords), _lib.ptr(state.meta),
                   caches, _lib.ptr(state._dev_counters), flags, stream_handle())
     else:
         _lib.call("cvb_partial_contract", _lib.C.byref(state.desc), _lib.ptr(state.f1.values),

@@ -68,8 +68,13 @@ def test_partial_sizes_host_only():
     per = (C.c_int64 * 8)()
     _lib.call("cvb_partial_sizes", C.byref(d), C.byref(nt), C.byref(mi), per)
     assert nt.value == 68 * 120
-    assert mi.value == nt.value * 4 * 8
+    # per-level meta (8 ints per tile and level) + one 108-int plan record per tile
+    assert mi.value == nt.value * 4 * 8 + nt.value * 108
     assert per[0] == nt.value * 24 * 24 * 64
+    f1b = C.c_int64()
+    _lib.call("cvb_tc_sizes", C.byref(d), C.byref(f1b), per)
+    assert f1b.value == nt.value * (64 * 256 * 4 + 64)  # B images + query exponents
+    assert per[0] == 4 * 540 * 960 * 256 + 540 * 960  # hi/lo planes + cell exponents
 
 
 def test_status_mapping():

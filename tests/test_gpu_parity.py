@@ -56,6 +56,22 @@ def test_pyramid_bit_exact_large(cuda):
         assert np.array_equal(pyr.levels[lvl].values.cpu().numpy(), want[lvl])
 
 
+@pytest.mark.parametrize("shape", [(135, 241, 256), (37, 29, 20), (16, 16, 64)])
+def test_fused_tc_prepare_pyramid_bit_exact(cuda, shape):
+    """The tensor-core path builds pyramid levels >= 1 inside its operand
+    split (cvb_tc_prepare + CVB_PREP_POOL): bit-exact with pool2x2."""
+    rng = np.random.default_rng(1)
+    h, w, d = shape
+    f = lambda: cvb.FeatureMap(torch.from_numpy(
+        rng.standard_normal((h, w, d)).astype(np.float32)).to(cuda))
+    f1, f2 = f(), f()
+    st = cvb.init_state(f1, f2, cvb.LookupSpec(4, 3))
+    assert st.tc
+    want = O.pyramid(f2.values.cpu().numpy(), 3)
+    for lvl in range(3):
+        assert np.array_equal(st.pyramid.levels[lvl].values.cpu().numpy(), want[lvl])
+
+
 def test_floors_and_support_masks_bit_exact(golden, cuda):
     c = golden["floors/coords"]
     st_coords = cvb.CentroidField(torch.from_numpy(c).to(cuda))
@@ -339,3 +355,26 @@ def test_pipelined_tile_ranges_equal_single_launch(cuda):
         assert np.array_equal(a, b)
         want = O.lookup(sc.f1, sc.f2, coords, 4, 4)
         assert O.deviation(b, want, want) <= REF_GATE
+
+
+def test_tc_per_row_scaling_wide_dynamic_range(cuda):
+    """Rows spanning 2^-20 .. 2^20 in magnitude: every row carries its own
+    power-of-two scale through the fp16 split, so both gates hold per row."""
+    rng = np.random.default_rng(5)
+    h, w, d = 24, 40, 256
+    scale1 = np.exp2(rng.integers(-20, 21, size=(h, w, 1))).astype(np.float32)
+    scale2 = np.exp2(rng.integers(-20, 21, size=(h, w, 1))).astype(np.float32)
+    f1 = (rng.standard_normal((h, w, d)) * scale1).astype(np.float32)
+    f2 = (rng.standard_normal((h, w, d)) * scale2).astype(np.float32)
+    spec = cvb.LookupSpec(4, 2)
+    sc = cvb.gen_scenario(3, (h, w, 4), 2, spec, coords_dtype=np.float32)
+    s = cvb.CorrSampler(cvb.FeatureMap(torch.from_numpy(f1).to(cuda)),
+                        cvb.FeatureMap(torch.from_numpy(f2).to(cuda)), spec)
+    for c in sc.centroid_fields:
+        want = O.lookup(f1, f2, c, spec.radius, spec.levels)
+        got = s(cvb.CentroidField(torch.from_numpy(c).to(cuda))).numpy()
+        # per-query relative error against the query's own cost scale
+        err = np.abs(got - want).reshape(h * w, -1).max(axis=1)
+        ref = np.abs(want).reshape(h * w, -1).max(axis=1)
+        ok = ref > 0
+        assert np.all(err[ok] <= 1e-5 * (ref[ok] + np.finfo(np.float32).tiny) * 16)
