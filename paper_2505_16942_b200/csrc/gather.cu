@@ -435,7 +435,7 @@ int launch_gather_kernel(const PartialParams& P, float* out, bool strict, cudaSt
   static int fast = -1;
   if (fast < 0) {
     const char* e = getenv("CVB_GATHER_FAST");
-    fast = (e != nullptr && e[0] == '1') ? 1 : 0;
+    fast = (e == nullptr || e[0] != '0') ? 1 : 0;
   }
   if (!strict && P.radius == 4 && fast) return launch_gather_fast_r4(P, out, s);
   for (int l0 = 0; l0 < P.levels; l0 += gather::MAXL) {

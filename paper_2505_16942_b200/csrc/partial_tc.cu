@@ -223,33 +223,55 @@ __device__ __forceinline__ int row_exp(const float (&x)[8]) {
   return scale_exp(m);
 }
 
-// F1 -> per-tile B-operand images + query exponents
+// F1 -> per-tile B-operand images + query exponents.  One warp per (tile,
+// 8-query row group): lane (q, j) = (lane & 7, lane >> 3) owns k-groups
+// j, j+4, ..., so every store instruction writes 4 x 128 contiguous bytes of
+// the image and every load 8 x 128 contiguous bytes of F1.
 __global__ void __launch_bounds__(256) split_f1_kernel(const float* __restrict__ f1, int h1,
                                                        int w1, int d, int dp, int tiles_x,
                                                        int64_t n_tiles, bool vec,
                                                        uint8_t* __restrict__ out,
                                                        int8_t* __restrict__ exps) {
-  const int lane = threadIdx.x & 31, kgs = dp / 8;
+  const int lane = threadIdx.x & 31, kgs = dp / 8;  // kgs <= 32
+  const int q8 = lane & 7, j = lane >> 3;
   const int64_t tile_bytes = (int64_t)N * dp * 2 * 2;
-  const int64_t rows = n_tiles * N;
-  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
-       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int q = (int)(r % N);
-    const int64_t tile = r / N;
+  const int64_t groups = n_tiles * (N / 8);
+  for (int64_t gidx = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; gidx < groups;
+       gidx += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int rg = (int)(gidx % (N / 8));
+    const int64_t tile = gidx / (N / 8);
+    const int q = rg * 8 + q8;
     const int py = (int)(tile / tiles_x) * TQH + q / TQW, px = (int)(tile % tiles_x) * TQW + q % TQW;
-    float x[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (lane < kgs && py < h1 && px < w1) load8(f1 + ((int64_t)py * w1 + px) * d, d, lane, vec, x);
-    const int e = row_exp(x);
-    if (lane < kgs) {
+    const bool valid = py < h1 && px < w1;
+    const float* row = f1 + ((int64_t)py * w1 + px) * d;
+    float x[8][8];
+    float m = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int kg = 4 * i + j;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[i][e] = 0.f;
+      if (valid && kg < kgs) load8(row, d, kg, vec, x[i]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) m = fmaxf(m, fabsf(x[i][e]));
+    }
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+    const int ex = scale_exp(m);
+    const float sc = exp2_neg(-ex);
+    uint8_t* img = out + tile * tile_bytes;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int kg = 4 * i + j;
+      if (kg >= kgs) continue;
       uint4 hi, lo;
-      split8(x, exp2_neg(-e), hi, lo);
-      const int piece = lane / (KP / 8), kgi = lane % (KP / 8);
-      uint8_t* base = out + tile * tile_bytes + (int64_t)piece * B_PIECE +
-                      (q / 8) * (KP / 8 * 128) + kgi * 128 + (q % 8) * 16;
+      split8(x[i], sc, hi, lo);
+      const int piece = kg / (KP / 8), kgi = kg % (KP / 8);
+      uint8_t* base = img + (int64_t)piece * B_PIECE + rg * (KP / 8 * 128) + kgi * 128 + q8 * 16;
       *reinterpret_cast<uint4*>(base) = hi;
       *reinterpret_cast<uint4*>(base + B_HALF) = lo;
     }
-    if (lane == 0) exps[r] = (int8_t)e;
+    if (j == 0) exps[tile * N + q] = (int8_t)ex;
   }
 }
 
@@ -837,7 +859,7 @@ int cvb_tc_prepare(const cvb_partial_desc* desc, const float* f1, float* const* 
   const int64_t n_tiles = ceil_div(desc->h1, TQH) * tiles_x;
   bool vec = d % 4 == 0 && ((uintptr_t)f1 & 15) == 0;
   uint8_t* f1s = reinterpret_cast<uint8_t*>(f1_split);
-  tc::split_f1_kernel<<<prep_grid(n_tiles * tc::N), 256, 0, s>>>(
+  tc::split_f1_kernel<<<prep_grid(n_tiles * (tc::N / 8)), 256, 0, s>>>(
       f1, desc->h1, desc->w1, d, dp, tiles_x, n_tiles, vec, f1s,
       reinterpret_cast<int8_t*>(f1s + n_tiles * tc::N * dp * 4));
   if ((st = check_launch("tc_split_f1")) != CVB_OK) return st;
