@@ -364,10 +364,10 @@ def main():
         tc, tg = sum(kern["contract_ms"]), sum(kern["gather_ms"])
         gather_bytes = (out_bytes_iter + coord_bytes_iter) * n_iter
         gather_gbs = gather_bytes / (tg / 1e3) / 1e9
-        r_gather = {"kernel": "gather_kernel (partial gather / bilinear sampler)", "bound": "hbm",
+        r_gather = {"kernel": "gather_fast_kernel (partial gather / bilinear sampler)", "bound": "hbm",
                     "achieved": round(gather_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                     "frac": round(gather_gbs / hbm_peak, 4),
-                    "traffic": traffic.get("gather_kernel"),
+                    "traffic": traffic.get("gather_fast_kernel"),
                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})",
                     "alg_bytes_per_launch": gather_bytes / n_iter,
                     "avg_launch_ms": tg / n_iter, "share_of_step": round(tg / (tc + tg), 3)}
