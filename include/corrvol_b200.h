@@ -53,6 +53,9 @@ typedef enum {
 #define CVB_COORDS_F64 2      /* centroid field is float64 (else float32)   */
 #define CVB_NO_CACHE 4        /* partial sampler: recompute every iteration */
 #define CVB_PREP_POOL 8       /* cvb_tc_prepare: also build pyramid levels >= 1 */
+#define CVB_OUT_RAFT 16       /* partial sampler output in RAFT's CorrBlock layout:
+                                 channel-first [L * (2r+1)^2][H][W], window index
+                                 dx * (2r+1) + dy (fast r=4 sampler only) */
 
 #define CVB_MAX_LEVELS 8
 

@@ -13,12 +13,13 @@ from .dense import (PYRAMID_MODES, DenseCorrelationVolume, build_dense_volume,
                     build_feature_pyramid, build_volume_pyramid, estimate_dense_bytes,
                     lookup_dense, pool_volume, pooled_dims)
 from .ondemand import WorkCount, count_work_on_demand, lookup_on_demand
+from .raft import CorrBlock
 from .sampler import VARIANTS, CorrSampler
 from .scenario import SyntheticScenario, gen_scenario
 from .sparse import (DEFAULT_CACHE_CAP_BYTES, BlockStore, PaddedGrid, ProxyBlock,
                      SparseVolumeState, compute_block_indices, gather_proxy, init_state,
-                     memory_footprint, padded_extent, sample_iteration, sampled_block_mmm,
-                     set_computation_mask)
+                     memory_footprint, padded_extent, sample_iteration, sample_iteration_raft,
+                     sampled_block_mmm, set_computation_mask)
 from .types import (CacheLimitError, CentroidField, CorrvolError, CostMaps,
                     DimensionMismatchError, FeatureMap, FeaturePyramid, GatherMissError,
                     LookupSpec, WorkCounter)
@@ -31,11 +32,11 @@ __all__ = [
     "build_volume_pyramid", "estimate_dense_bytes", "lookup_dense", "pool_volume",
     "pooled_dims",
     "WorkCount", "count_work_on_demand", "lookup_on_demand",
-    "VARIANTS", "CorrSampler",
+    "VARIANTS", "CorrSampler", "CorrBlock",
     "SyntheticScenario", "gen_scenario",
     "DEFAULT_CACHE_CAP_BYTES", "BlockStore", "PaddedGrid", "ProxyBlock", "SparseVolumeState",
     "compute_block_indices", "gather_proxy", "init_state", "memory_footprint", "padded_extent",
-    "sample_iteration", "sampled_block_mmm", "set_computation_mask",
+    "sample_iteration", "sample_iteration_raft", "sampled_block_mmm", "set_computation_mask",
     "CacheLimitError", "CentroidField", "CorrvolError", "CostMaps", "DimensionMismatchError",
     "FeatureMap", "FeaturePyramid", "GatherMissError", "LookupSpec", "WorkCounter",
 ]

@@ -27,6 +27,7 @@ CVB_STRICT = 1
 CVB_COORDS_F64 = 2
 CVB_NO_CACHE = 4
 CVB_PREP_POOL = 8
+CVB_OUT_RAFT = 16
 
 MAX_LEVELS = 8
 TILE_H = 8

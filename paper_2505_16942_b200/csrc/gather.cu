@@ -437,7 +437,8 @@ int launch_gather_kernel(const PartialParams& P, float* out, bool strict, cudaSt
     const char* e = getenv("CVB_GATHER_FAST");
     fast = (e == nullptr || e[0] != '0') ? 1 : 0;
   }
-  if (!strict && P.radius == 4 && fast) return launch_gather_fast_r4(P, out, s);
+  if (!strict && P.radius == 4 && (fast || P.out_raft)) return launch_gather_fast_r4(P, out, s);
+  CVB_REQUIRE(!P.out_raft, "CVB_OUT_RAFT needs the fast-arithmetic r=4 sampler");
   for (int l0 = 0; l0 < P.levels; l0 += gather::MAXL) {
     const int nl = min(gather::MAXL, P.levels - l0);
     if (P.radius == 4) {

@@ -143,8 +143,28 @@ __global__ void __launch_bounds__(WARPS * 32, 2) gather_fast_kernel(PartialParam
     }
   }
   __syncwarp();
-  // ---- write back: the row's block out[row0 .. row0+8) x [levels] x 81 ----
-  if (nlev == P.levels && vmask == 0xFFu && (P.levels * KK) % 4 == 0 &&
+  // ---- write back ----
+  if (P.out_raft) {
+    // RAFT CorrBlock layout: out[(l * 81 + dx * 9 + dy) * H * W + pixel]; per
+    // window index the row's 8 queries are 32 contiguous bytes
+    const int64_t hw = (int64_t)P.h1 * P.w1;
+    const bool vec4 = vmask == 0xFFu && (row0 & 3) == 0 && (hw & 3) == 0 &&
+                      ((uintptr_t)out & 15) == 0;
+    for (int e = lane; e < nlev * KK * 2; e += 32) {
+      const int hq = e & 1, lt = e >> 1;
+      const int l_ = lt / KK, t = lt - l_ * KK;
+      const int dy = t / K, dx = t - dy * K;
+      float* dst = out + ((int64_t)(level0 + l_) * KK + dx * K + dy) * hw + row0 + 4 * hq;
+      const float* src = O + (4 * hq) * nlev * KK + lt;
+      if (vec4) {
+        *reinterpret_cast<float4*>(dst) =
+            make_float4(src[0], src[nlev * KK], src[2 * nlev * KK], src[3 * nlev * KK]);
+      } else {
+        for (int k = 0; k < 4; ++k)
+          if ((vmask >> (4 * hq + k)) & 1u) dst[k] = src[k * nlev * KK];
+      }
+    }
+  } else if (nlev == P.levels && vmask == 0xFFu && (P.levels * KK) % 4 == 0 &&
       ((uintptr_t)out & 15) == 0) {
     // one contiguous 16-byte-aligned block of 8 * L * 81 floats
     const int n4 = TQW * nlev * KK / 4;

@@ -174,6 +174,7 @@ __attribute__((visibility("hidden"))) int cvb_internal_build_params(
   P.f64 = flags & CVB_COORDS_F64;
   P.normalize = scale != 1.0f;
   P.no_cache = flags & CVB_NO_CACHE;
+  P.out_raft = flags & CVB_OUT_RAFT;
   P.vec = vec;
   CVB_REQUIRE(P.n_tiles <= 2147483647LL, "too many tiles");
   P.tile0 = desc->tile_begin > 0 ? desc->tile_begin : 0;

@@ -24,6 +24,7 @@ struct PartialParams {
   int64_t tile0, ntile;  // range handled by this launch
   float scale;
   bool f64, normalize, no_cache, vec;
+  bool out_raft;         // CVB_OUT_RAFT output layout
 };
 
 struct Box {

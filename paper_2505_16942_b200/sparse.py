@@ -688,6 +688,29 @@ def sample_iteration(state: SparseVolumeState, centroids: CentroidField,
     return CostMaps(values=out, radius=spec.radius)
 
 
+def sample_iteration_raft(state: SparseVolumeState, centroids: CentroidField,
+                          out: torch.Tensor) -> torch.Tensor:
+    """One lookup iteration written straight into RAFT's CorrBlock layout:
+    out [L * (2r+1)^2, H, W], window index dx * (2r+1) + dy (the order RAFT's
+    meshgrid(dy, dx) delta produces), by the sampler kernel itself
+    (CVB_OUT_RAFT; fast r=4 tile path)."""
+    if state.mode != "tile" or state.strict or state.spec.radius != 4:
+        raise ValueError("CVB_OUT_RAFT needs a fast-arithmetic r=4 tile-mode state")
+    _check_grid(state, centroids)
+    spec, f1 = state.spec, state.f1
+    if out.shape != (spec.levels * spec.window ** 2, f1.height, f1.width) or \
+            out.dtype != torch.float32 or not out.is_contiguous():
+        raise ValueError("out must be a contiguous float32 [L*(2r+1)^2, H, W] tensor")
+    flags = coords_flags(centroids, False)
+    if not state.cache_enabled:
+        flags |= _lib.CVB_NO_CACHE
+    f2s, caches = _contract_args(state, centroids, flags)
+    _contract(state, centroids, flags, f2s, caches)
+    _gather(state, centroids, flags | _lib.CVB_OUT_RAFT, f2s, caches, out)
+    state.iteration += 1
+    return out
+
+
 def memory_footprint(state: SparseVolumeState) -> Dict:
     """Byte accounting of the sampler state (sparse.py:455-496).
 
