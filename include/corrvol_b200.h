@@ -213,6 +213,16 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
                             float* const* cache_levels_host, unsigned long long* counters,
                             int32_t flags, void* stream);
 
+/* ---- cascaded-init flow resample (flowio.py:151-199) ------------------- */
+/* Output dims round(dim * scale) half-up, each >= 1 (flowio.py:164-168). */
+int cvb_resample_dims(int32_t h, int32_t w, double scale, int32_t* out_h, int32_t* out_w);
+/* Bilinear resample of a [h][w][2] float32 flow field to [out_h][out_w][2]:
+ * src = (out + 0.5) / scale - 0.5 clamped to the grid, fp64 combine
+ * ((v00 w00 + v01 w01) + v10 w10) + v11 w11, magnitudes times scale;
+ * bit-identical to resample_flow (flowio.py:151-184). */
+int cvb_resample_flow(const float* in, int32_t h, int32_t w, double scale, float* out,
+                      int32_t out_h, int32_t out_w, void* stream);
+
 /* ---- reference block-sparse state (sparse.py:262-309) ------------------- */
 
 /* Computation mask of one level as a bitmask: row s (source tile) has

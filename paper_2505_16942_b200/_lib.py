@@ -84,6 +84,8 @@ SIGNATURES = {
                                  _i32, _p]),
     "cvb_partial_contract_tc": (C.c_int, [C.POINTER(PartialDesc), _p, C.POINTER(_p), _p,
                                           C.POINTER(_p), _p, _p, C.POINTER(_p), _p, _i32, _p]),
+    "cvb_resample_dims": (C.c_int, [_i32, _i32, C.c_double, C.POINTER(_i32), C.POINTER(_i32)]),
+    "cvb_resample_flow": (C.c_int, [_p, _i32, _i32, C.c_double, _p, _i32, _i32, _p]),
     "cvb_computation_mask": (C.c_int, [_p, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _p,
                                        _i64, _p]),
     "cvb_block_indices_workspace": (_i64, [_i64]),
