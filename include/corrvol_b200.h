@@ -213,6 +213,24 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
                             float* const* cache_levels_host, unsigned long long* counters,
                             int32_t flags, void* stream);
 
+/* ---- access recorder / block occupancy (analyzer.py:31-116) ------------- */
+#define CVB_ACCESS_NO_TRIM 32 /* count the full (2r+2)^2 support even where the
+                                 last row / column has zero bilinear weight */
+/* first_touch[i] += number of (query, target cell) pairs first touched in
+ * iteration i (cells with nonzero bilinear weight, unpadded level grid); the
+ * sum over i is the size of the reference's AccessLog for the level.
+ * coords_iters_host: n_iter (<= 64) device pointers to [h1][w1][2] centroids.
+ * first_touch: device, n_iter counters (caller zeroes). */
+int cvb_access_union(const void* const* coords_iters_host, int32_t n_iter, int32_t h1, int32_t w1,
+                     int32_t level, int32_t radius, int32_t th, int32_t tw, int32_t flags,
+                     unsigned long long* first_touch, void* stream);
+/* ORs one iteration's touched (source group, target group) pairs into a
+ * [n_src_groups][words_per_row] uint32 bitmask; patch_major selects B x B
+ * spatial tiles, else B^2 consecutive raster indices (analyzer.py:83-97). */
+int cvb_access_blocks(const void* coords, int32_t h1, int32_t w1, int32_t level, int32_t radius,
+                      int32_t th, int32_t tw, int32_t block, int32_t patch_major, int32_t flags,
+                      uint32_t* mask, int64_t words_per_row, void* stream);
+
 /* ---- cascaded-init flow resample (flowio.py:151-199) ------------------- */
 /* Output dims round(dim * scale) half-up, each >= 1 (flowio.py:164-168). */
 int cvb_resample_dims(int32_t h, int32_t w, double scale, int32_t* out_h, int32_t* out_w);

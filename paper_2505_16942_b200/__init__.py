@@ -12,6 +12,7 @@ from ._backend import available_backends, default_backend, get_kernels
 from .dense import (PYRAMID_MODES, DenseCorrelationVolume, build_dense_volume,
                     build_feature_pyramid, build_volume_pyramid, estimate_dense_bytes,
                     lookup_dense, pool_volume, pooled_dims)
+from .analyzer import LevelAccess, record_occupancy
 from .flow import cascaded_init, resample_flow
 from .ondemand import WorkCount, count_work_on_demand, lookup_on_demand
 from .raft import CorrBlock
@@ -33,7 +34,7 @@ __all__ = [
     "build_volume_pyramid", "estimate_dense_bytes", "lookup_dense", "pool_volume",
     "pooled_dims",
     "WorkCount", "count_work_on_demand", "lookup_on_demand",
-    "cascaded_init", "resample_flow",
+    "cascaded_init", "resample_flow", "LevelAccess", "record_occupancy",
     "VARIANTS", "CorrSampler", "CorrBlock",
     "SyntheticScenario", "gen_scenario",
     "DEFAULT_CACHE_CAP_BYTES", "BlockStore", "PaddedGrid", "ProxyBlock", "SparseVolumeState",

@@ -28,6 +28,7 @@ CVB_COORDS_F64 = 2
 CVB_NO_CACHE = 4
 CVB_PREP_POOL = 8
 CVB_OUT_RAFT = 16
+CVB_ACCESS_NO_TRIM = 32
 
 MAX_LEVELS = 8
 TILE_H = 8
@@ -84,6 +85,10 @@ SIGNATURES = {
                                  _i32, _p]),
     "cvb_partial_contract_tc": (C.c_int, [C.POINTER(PartialDesc), _p, C.POINTER(_p), _p,
                                           C.POINTER(_p), _p, _p, C.POINTER(_p), _p, _i32, _p]),
+    "cvb_access_union": (C.c_int, [C.POINTER(_p), _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
+                                   _p, _p]),
+    "cvb_access_blocks": (C.c_int, [_p, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _p,
+                                    _i64, _p]),
     "cvb_resample_dims": (C.c_int, [_i32, _i32, C.c_double, C.POINTER(_i32), C.POINTER(_i32)]),
     "cvb_resample_flow": (C.c_int, [_p, _i32, _i32, C.c_double, _p, _i32, _i32, _p]),
     "cvb_computation_mask": (C.c_int, [_p, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _p,
