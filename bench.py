@@ -38,6 +38,7 @@ CONFIGS = {
     "C2": (135, 240, 256, 4, 4, 32, False),
     "C3": (270, 480, 256, 4, 4, 12, True),
     "C4": (540, 960, 256, 4, 4, 12, False),
+    "C5": (270, 480, 256, 4, 4, 12, True),   # per pair; --batch pairs (seeds 0..B-1)
 }
 METRIC = "corr-lookup ms/iter + peak HBM at 8K (L=4,r=4,D=256) at 1/2/4/8 B200 vs roofline"
 FP32_LANES_PER_SM = 128
@@ -53,6 +54,9 @@ def parse():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="C4")
     ap.add_argument("--variant", choices=["partial", "ondemand", "dense"], default="partial")
     ap.add_argument("--strict", action="store_true", help="reference-exact arithmetic")
+    ap.add_argument("--batch", type=int, default=8, help="C5: image pairs in the batch")
+    ap.add_argument("--gather", action="store_true",
+                    help="C5 at N>1: all-gather every pair's costs to every rank per iteration")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compare", action="store_true")
@@ -243,6 +247,9 @@ def main():
         return
     if args.impl == "reference":
         run_reference_arm(args)
+        return
+    if args.config == "C5":
+        run_batch(args)
         return
 
     import torch
@@ -514,6 +521,87 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_batch(args) -> None:
+    """C5: a batch of 4K pairs (SEA-RAFT sampler config, normalize=True), batch
+    slices per rank (no data-path collective); --gather adds the per-iteration
+    NCCL all-gather of the sampled costs, timed separately."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_16942_b200 as cvb
+    from paper_2505_16942_b200.parallel import batch_slices, gather_bands
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    h, w, d, r, levels, n_iter, norm = CONFIGS["C5"]
+    spec = cvb.LookupSpec(r, levels, norm)
+    a, b = batch_slices(args.batch, world)[rank]
+    scs = [cvb.gen_scenario(s, (h, w, d), n_iter, spec, coords_dtype=np.float32)
+           for s in range(a, b)]
+    f1 = torch.stack([torch.from_numpy(sc.f1) for sc in scs]).to(dev)
+    f2 = torch.stack([torch.from_numpy(sc.f2) for sc in scs]).to(dev)
+    coords = [torch.stack([torch.from_numpy(sc.centroid_fields[i]) for sc in scs]).to(dev)
+              for i in range(n_iter)]
+    k = spec.window
+    out = torch.empty((b - a, h, w, levels, k, k), dtype=torch.float32, device=dev)
+    slices = batch_slices(args.batch, world)
+    t_gather = [0.0]
+
+    def step():
+        s = cvb.BatchCorrSampler(f1, f2, spec, strict=args.strict)
+        for c in coords:
+            s(c, out=out)
+            if args.gather and world > 1:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                gather_bands(out, slices)
+                e1.record()
+                e1.synchronize()
+                t_gather[0] += e0.elapsed_time(e1)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_gather[0] = 0.0
+    torch.cuda.reset_peak_memory_stats(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    peak = torch.cuda.max_memory_allocated(dev)
+    if world > 1:
+        t = torch.tensor([ms, float(peak)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, peak = float(t[0]), int(t[1])
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC + " [C5 batch sweep]", "value": round(ms / n_iter, 4),
+            "unit": "ms/iter", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (gen_scenario seeds 0..B-1)",
+            "config": {"workload": f"C5 batch {args.batch} x {h}x{w} D={d} L={levels} r={r} "
+                                   f"{n_iter} iterations (normalize)",
+                       "parallelism": f"batch slices x{world}",
+                       "l2": "inputs larger than L2"},
+            "lookups_per_s": round(args.batch * h * w * n_iter / (ms / 1e3), 1),
+            "peak_hbm_bytes_per_gpu": peak,
+            "allgather_ms_per_step": round(t_gather[0] / args.steps, 3) if args.gather else None,
+            "e2e": None, "gpu_launches": None}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

@@ -16,7 +16,7 @@ from .analyzer import LevelAccess, record_occupancy
 from .flow import cascaded_init, resample_flow
 from .ondemand import WorkCount, count_work_on_demand, lookup_on_demand
 from .raft import CorrBlock
-from .sampler import VARIANTS, CorrSampler
+from .sampler import VARIANTS, BatchCorrSampler, CorrSampler
 from .scenario import SyntheticScenario, gen_scenario
 from .sparse import (DEFAULT_CACHE_CAP_BYTES, BlockStore, PaddedGrid, ProxyBlock,
                      SparseVolumeState, compute_block_indices, gather_proxy, init_state,
@@ -35,7 +35,7 @@ __all__ = [
     "pooled_dims",
     "WorkCount", "count_work_on_demand", "lookup_on_demand",
     "cascaded_init", "resample_flow", "LevelAccess", "record_occupancy",
-    "VARIANTS", "CorrSampler", "CorrBlock",
+    "VARIANTS", "CorrSampler", "BatchCorrSampler", "CorrBlock",
     "SyntheticScenario", "gen_scenario",
     "DEFAULT_CACHE_CAP_BYTES", "BlockStore", "PaddedGrid", "ProxyBlock", "SparseVolumeState",
     "compute_block_indices", "gather_proxy", "init_state", "memory_footprint", "padded_extent",

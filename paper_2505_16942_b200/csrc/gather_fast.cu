@@ -17,7 +17,7 @@
 //     of the [H,W,L,9,9] cost map) are staged in shared memory and written with
 //     128-bit stores.
 // Levels whose box overflowed the cache window are evaluated by direct dot
-// products (gather.cu semantics).
+// products, the warp cooperating on each query's window (gather.cu semantics).
 #include "partial.cuh"
 
 namespace cvb {
@@ -29,7 +29,69 @@ constexpr int R = 4, K = 9, KK = 81, S = 10;
 
 struct Shared {
   float outs[WARPS][TQW * MAXL * KK];  // 10,368 B per warp
+  float patch[WARPS][S * S];           // overflow path: one query's window
 };
+
+// Overflowed tile-level (its box exceeded the cache window): the warp
+// evaluates each query's (2r+2)^2 window by direct dot products — lanes split
+// the 100 cells, four independent 128-bit-load dot chains per lane — then
+// combines the taps from the staged patch (gather.cu semantics, fmaf dots).
+__device__ __noinline__ void overflow_level(const float* f1, const float* f2, int th, int tw,
+                                            int d, bool vec, int64_t row0, unsigned vmask,
+                                            int ay, int ax, Weights32 w, int l_, int nlev,
+                                            float* patch, float* O, int lane) {
+  for (int qq = 0; qq < TQW; ++qq) {
+    const int src = 8 * l_ + qq;
+    const int qay = __shfl_sync(0xffffffffu, ay, src), qax = __shfl_sync(0xffffffffu, ax, src);
+    Weights32 qw;
+    qw.w00 = __shfl_sync(0xffffffffu, w.w00, src);
+    qw.w01 = __shfl_sync(0xffffffffu, w.w01, src);
+    qw.w10 = __shfl_sync(0xffffffffu, w.w10, src);
+    qw.w11 = __shfl_sync(0xffffffffu, w.w11, src);
+    if (!((vmask >> qq) & 1u)) continue;
+    const float* a = f1 + (row0 + qq) * (int64_t)d;
+    const float* b[4];
+    bool in[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = lane + 32 * j;
+      const int cy = qay - R + c / S, cx = qax - R + c % S;
+      in[j] = c < S * S && cy >= 0 && cy < th && cx >= 0 && cx < tw;
+      b[j] = in[j] ? f2 + ((int64_t)cy * tw + cx) * d : a;
+    }
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    if (vec) {
+      for (int k = 0; k < d; k += 4) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(a + k));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 y = __ldg(reinterpret_cast<const float4*>(b[j] + k));
+          acc[j] = fmaf(x.x, y.x, acc[j]);
+          acc[j] = fmaf(x.y, y.y, acc[j]);
+          acc[j] = fmaf(x.z, y.z, acc[j]);
+          acc[j] = fmaf(x.w, y.w, acc[j]);
+        }
+      }
+    } else {
+      for (int k = 0; k < d; ++k) {
+        const float x = __ldg(a + k);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = fmaf(x, __ldg(b[j] + k), acc[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (lane + 32 * j < S * S) patch[lane + 32 * j] = in[j] ? acc[j] : 0.f;
+    __syncwarp();
+    float* o = O + (qq * nlev + l_) * KK;
+    for (int t = lane; t < KK; t += 32) {
+      const int dy = t / K, dx = t - dy * K;
+      o[t] = combine32(patch[dy * S + dx], patch[dy * S + dx + 1], patch[(dy + 1) * S + dx],
+                       patch[(dy + 1) * S + dx + 1], qw);
+    }
+    __syncwarp();
+  }
+}
 
 __global__ void __launch_bounds__(WARPS * 32, 2) gather_fast_kernel(PartialParams P, float* out,
                                                                     int level0, int nlev) {
@@ -84,6 +146,11 @@ __global__ void __launch_bounds__(WARPS * 32, 2) gather_fast_kernel(PartialParam
     qw.w10 = __shfl_sync(0xffffffffu, w.w10, src);
     qw.w11 = __shfl_sync(0xffffffffu, w.w11, src);
     const int th = P.th[l], tw = P.tw[l];
+    if (st == ST_OVERFLOW) {  // warp-uniform
+      overflow_level(P.f1, P.f2[l], P.th[l], P.tw[l], P.d, P.vec, row0, vmask, ay, ax, w, l_,
+                     nlev, sm.patch[warp], O, lane);
+      continue;
+    }
     float v[4][S];
     if (active) {
       const int y0 = qay - R + 3 * p, x0 = qax - R;
@@ -108,24 +175,6 @@ __global__ void __launch_bounds__(WARPS * 32, 2) gather_fast_kernel(PartialParam
             const int gx = x0 + i;
             v[j][i] = (rin && gx >= 0 && gx < tw) ? __ldg(prow + sx * TQW) : 0.f;
             if (++sx == cw) sx = 0;
-          }
-        }
-      } else if (st == ST_OVERFLOW) {
-        const float* a = P.f1 + (row0 + q) * (int64_t)P.d;
-        const float* f2 = P.f2[l];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int gy = y0 + j;
-#pragma unroll
-          for (int i = 0; i < S; ++i) {
-            const int gx = x0 + i;
-            float acc = 0.f;
-            if (gy >= 0 && gy < th && gx >= 0 && gx < tw) {
-              const float* b = f2 + ((int64_t)gy * tw + gx) * P.d;
-#pragma unroll 1
-              for (int k = 0; k < P.d; ++k) acc = fmaf(__ldg(a + k), __ldg(b + k), acc);
-            }
-            v[j][i] = acc;
           }
         }
       } else {

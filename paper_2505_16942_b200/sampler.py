@@ -84,3 +84,40 @@ class CorrSampler:
             return self.volume.nbytes() + self.f1.values.numel() * 4 + \
                 self.f2.values.numel() * 4
         return feats
+
+
+class BatchCorrSampler:
+    """A batch of independent image pairs (C5: batched 4K sweep).
+
+    fmaps1 / fmaps2: [B, H, W, D]; `__call__(coords [B, H, W, 2])` returns
+    [B, H, W, L, 2r+1, 2r+1].  Each pair keeps its own state (the reference
+    has no batching), so pairs shard across ranks with no
+    data-path collective (`parallel.batch_slices`); `parallel.gather_bands`
+    all-gathers the per-rank slices when a caller needs every pair's costs
+    on every rank.
+    """
+
+    def __init__(self, fmaps1: torch.Tensor, fmaps2: torch.Tensor, spec: LookupSpec,
+                 variant: str = "partial", **kwargs):
+        if fmaps1.dim() != 4 or fmaps1.shape != fmaps2.shape:
+            raise ValueError("fmaps must both be [B, H, W, D] with equal shapes")
+        self.spec = spec
+        self.samplers = [CorrSampler(FeatureMap(fmaps1[b], check=False),
+                                     FeatureMap(fmaps2[b], check=False), spec, variant=variant,
+                                     check=False, **kwargs)
+                         for b in range(fmaps1.shape[0])]
+
+    def __len__(self) -> int:
+        return len(self.samplers)
+
+    def __call__(self, coords: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        b, h, w = coords.shape[:3]
+        if b != len(self.samplers):
+            raise ValueError(f"coords batch {b} != {len(self.samplers)} pairs")
+        k = self.spec.window
+        if out is None:
+            out = torch.empty((b, h, w, self.spec.levels, k, k), dtype=torch.float32,
+                              device=coords.device)
+        for i, s in enumerate(self.samplers):
+            s(CentroidField(coords[i], check=False), out=out[i])
+        return out

@@ -45,7 +45,7 @@ MODES = ("tile", "block")
 #: An 8x8 tile's support box is >= (8/2^l + 2r+1) cells per axis; the window
 #: leaves room for flow divergence.  Boxes that do not fit are evaluated
 #: directly for that iteration (never wrong, only slower).
-DEFAULT_TILE_CAPS = (28, 20, 16, 16, 16, 16, 16, 16)
+DEFAULT_TILE_CAPS = (32, 20, 16, 16, 16, 16, 16, 16)
 
 
 def _default_cache_cap() -> int:

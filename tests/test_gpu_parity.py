@@ -378,3 +378,40 @@ def test_tc_per_row_scaling_wide_dynamic_range(cuda):
         ref = np.abs(want).reshape(h * w, -1).max(axis=1)
         ok = ref > 0
         assert np.all(err[ok] <= 1e-5 * (ref[ok] + np.finfo(np.float32).tiny) * 16)
+
+
+@pytest.mark.parametrize("strict", [False, True])
+def test_row_bands_concatenate_to_full_frame_bitwise(cuda, strict):
+    """query-row bands (starts aligned to the 8-row tile) against a
+    replicated fmap2 reproduce the single-GPU frame bit for bit."""
+    from paper_2505_16942_b200.parallel import row_bands
+
+    spec = cvb.LookupSpec(4, 4)
+    h, w, d = 70, 90, 64
+    sc = cvb.gen_scenario(6, (h, w, d), 3, spec, coords_dtype=np.float32)
+    f1 = torch.from_numpy(sc.f1).to(cuda)
+    f2 = cvb.FeatureMap(torch.from_numpy(sc.f2).to(cuda))
+    full = cvb.CorrSampler(cvb.FeatureMap(f1), f2, spec, strict=strict)
+    bands = [cvb.CorrSampler(cvb.FeatureMap(f1[a:b].contiguous()), f2, spec, strict=strict)
+             for a, b in row_bands(h, 3)]
+    for c in sc.centroid_fields:
+        ct = torch.from_numpy(c).to(cuda)
+        want = full(cvb.CentroidField(ct)).numpy()
+        got = np.concatenate([s(cvb.CentroidField(ct[a:b].contiguous())).numpy()
+                              for s, (a, b) in zip(bands, row_bands(h, 3))])
+        assert np.array_equal(got, want)
+
+
+def test_batch_sampler_equals_per_pair(cuda):
+    spec = cvb.LookupSpec(4, 3)
+    scs = [cvb.gen_scenario(s, (24, 40, 32), 2, spec, coords_dtype=np.float32) for s in (1, 2, 3)]
+    f1 = torch.stack([torch.from_numpy(s.f1) for s in scs]).to(cuda)
+    f2 = torch.stack([torch.from_numpy(s.f2) for s in scs]).to(cuda)
+    batch = cvb.BatchCorrSampler(f1, f2, spec)
+    singles = [cvb.CorrSampler(cvb.FeatureMap(f1[i]), cvb.FeatureMap(f2[i]), spec)
+               for i in range(3)]
+    for it in range(2):
+        coords = torch.stack([torch.from_numpy(s.centroid_fields[it]) for s in scs]).to(cuda)
+        got = batch(coords).cpu().numpy()
+        for i in range(3):
+            assert np.array_equal(got[i], singles[i](cvb.CentroidField(coords[i])).numpy())
