@@ -8,11 +8,11 @@
 //   * one warp per query row of a tile (8 queries), all levels (<= 4 per
 //     launch); lane (q, l) = (lane & 7, lane >> 3) derives the anchor and
 //     weights of query q at level l once (the four levels in parallel);
-//   * taps: lane (q, p), p < 3, owns tap rows 3p..3p+2 of query q: it loads
-//     the 4 x 10 patch values they need from the cache plane ([slot][8 queries],
-//     so the 8 lanes of one (p) read one 32-byte sector per cell), zero outside
-//     the level grid, and combines them in registers (canonical fp32 combine,
-//     pre-scaled weights);
+//   * taps: lane (q, l) owns query q at level l: three passes of 3 tap rows,
+//     each loading the 4 x 10 patch values it needs from the cache plane
+//     ([slot][8 queries], 32-byte sectors shared by the row's queries through
+//     L1) into registers, zero outside the level grid, and combining them
+//     (canonical fp32 combine, pre-scaled weights);
 //   * the row's outputs (8 queries x L levels x 81 taps, one contiguous block
 //     of the [H,W,L,9,9] cost map) are staged in shared memory and written with
 //     128-bit stores.
@@ -131,64 +131,52 @@ __global__ void __launch_bounds__(WARPS * 32, 2) gather_fast_kernel(PartialParam
   if (vmask == 0) return;
   const int64_t row0 = (int64_t)py * P.w1 + tile_x * TQW;
   float* O = sm.outs[warp];  // [q][nlev][81]
-  const int p = lane >> 3;   // tap-row group; lanes 24..31 idle in the combine
-  const bool active = p < 3 && ((vmask >> q) & 1u);
-
+  // overflowed levels: warp-cooperative direct dots (warp-uniform loop)
   for (int l_ = 0; l_ < nlev; ++l_) {
-    const int l = level0 + l_;
-    const int src = 8 * l_ + q;
-    const int qay = __shfl_sync(0xffffffffu, ay, src);
-    const int qax = __shfl_sync(0xffffffffu, ax, src);
-    const int st = __shfl_sync(0xffffffffu, status, 8 * l_);
-    Weights32 qw;
-    qw.w00 = __shfl_sync(0xffffffffu, w.w00, src);
-    qw.w01 = __shfl_sync(0xffffffffu, w.w01, src);
-    qw.w10 = __shfl_sync(0xffffffffu, w.w10, src);
-    qw.w11 = __shfl_sync(0xffffffffu, w.w11, src);
-    const int th = P.th[l], tw = P.tw[l];
-    if (st == ST_OVERFLOW) {  // warp-uniform
-      overflow_level(P.f1, P.f2[l], P.th[l], P.tw[l], P.d, P.vec, row0, vmask, ay, ax, w, l_,
-                     nlev, sm.patch[warp], O, lane);
-      continue;
+    if (__shfl_sync(0xffffffffu, status, 8 * l_) == ST_OVERFLOW)
+      overflow_level(P.f1, P.f2[level0 + l_], P.th[level0 + l_], P.tw[level0 + l_], P.d, P.vec,
+                     row0, vmask, ay, ax, w, l_, nlev, sm.patch[warp], O, lane);
+  }
+  // every lane (q, l) combines the 81 taps of query q at level l, three tap
+  // rows per pass from 4 x 10 cache values loaded into registers
+  if (li < nlev && qvalid && status != ST_OVERFLOW) {
+    const int l = level0 + li;
+    const int th = P.th[l], tw = P.tw[l], ch = P.ch[l], cw = P.cw[l];
+    const float* plane = P.cache[l] + ((tile * TQH + qrow) * (int64_t)(ch * cw)) * TQW + q;
+    const int x0 = ax - R;
+    int xs = x0 % cw;
+    if (xs < 0) xs += cw;
+    // toroidal slot offsets and in-grid flags of the 10 patch columns
+    int colofs[S];
+    bool colin[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      colofs[i] = xs * TQW;
+      colin[i] = x0 + i >= 0 && x0 + i < tw;
+      if (++xs == cw) xs = 0;
     }
-    float v[4][S];
-    if (active) {
-      const int y0 = qay - R + 3 * p, x0 = qax - R;
-      if (st == ST_OK) {
-        const int ch = P.ch[l], cw = P.cw[l];
-        const float* plane = P.cache[l] + ((tile * TQH + qrow) * (int64_t)(ch * cw)) * TQW + q;
-        // toroidal column offsets of the 10 patch columns (in-grid ones only)
-        int xs = x0 % cw;
-        if (xs < 0) xs += cw;
-        int ys = y0 % ch;
-        if (ys < 0) ys += ch;
+    float* o = O + (q * nlev + li) * KK;
+#pragma unroll 1
+    for (int pass = 0; pass < 3; ++pass) {
+      const int y0 = ay - R + 3 * pass;
+      int sy = y0 % ch;
+      if (sy < 0) sy += ch;
+      float v[4][S];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int gy = y0 + j;
-          const bool rin = gy >= 0 && gy < th;
-          int sy = ys + j;
-          if (sy >= ch) sy -= ch;
-          const float* prow = plane + (int64_t)(sy * cw) * TQW;
-          int sx = xs;
+      for (int j = 0; j < 4; ++j) {
+        const int gy = y0 + j;
+        const bool rin = status == ST_OK && gy >= 0 && gy < th;
+        const float* prow = plane + (int64_t)(sy * cw) * TQW;
 #pragma unroll
-          for (int i = 0; i < S; ++i) {
-            const int gx = x0 + i;
-            v[j][i] = (rin && gx >= 0 && gx < tw) ? __ldg(prow + sx * TQW) : 0.f;
-            if (++sx == cw) sx = 0;
-          }
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int i = 0; i < S; ++i) v[j][i] = 0.f;
+        for (int i = 0; i < S; ++i) v[j][i] = (rin && colin[i]) ? __ldg(prow + colofs[i]) : 0.f;
+        if (++sy == ch) sy = 0;
       }
-      float* o = O + (q * nlev + l_) * KK + 3 * p * K;
 #pragma unroll
       for (int j = 0; j < 3; ++j)
 #pragma unroll
         for (int i = 0; i < K; ++i)
-          o[j * K + i] = combine32(v[j][i], v[j][i + 1], v[j + 1][i], v[j + 1][i + 1], qw);
+          o[(3 * pass + j) * K + i] =
+              combine32(v[j][i], v[j][i + 1], v[j + 1][i], v[j + 1][i + 1], w);
     }
   }
   __syncwarp();
