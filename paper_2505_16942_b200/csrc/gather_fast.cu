@@ -97,6 +97,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2) gather_fast_kernel(PartialParam
                                                                     int level0, int nlev) {
   extern __shared__ __align__(16) uint8_t g_smem[];
   Shared& sm = *reinterpret_cast<Shared*>(g_smem);
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tile = P.tile0 + blockIdx.x;
   const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
@@ -231,7 +233,8 @@ int launch_gather_fast_r4(const PartialParams& P, float* out, cudaStream_t s) {
   }
   for (int l0 = 0; l0 < P.levels; l0 += gfast::MAXL) {
     const int nl = min(gfast::MAXL, P.levels - l0);
-    gfast::gather_fast_kernel<<<(unsigned)P.ntile, gfast::WARPS * 32, smem, s>>>(P, out, l0, nl);
+    launch_pdl(gfast::gather_fast_kernel, dim3((unsigned)P.ntile), dim3(gfast::WARPS * 32), smem,
+               s, P, out, l0, nl);
     const int st = check_launch("partial_gather_fast");
     if (st != CVB_OK) return st;
   }

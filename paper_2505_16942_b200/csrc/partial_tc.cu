@@ -463,6 +463,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = C.tmem;
+  pdl_trigger();
+  pdl_wait();  // the plan records, meta and cache of earlier launches are complete
 
   if (warp == 0) {
     // ---------------- B producer: F1 pieces ----------------
@@ -694,6 +696,8 @@ constexpr int PLAN_WARPS = 8;
 
 __global__ void __launch_bounds__(PLAN_WARPS * 32) plan_kernel(PartialParams P) {
   __shared__ unsigned long long s_cnt[4];
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0ULL;
   __syncthreads();
@@ -934,11 +938,12 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  tcp::plan_kernel<<<(unsigned)ceil_div(T.P.ntile, tcp::PLAN_WARPS), tcp::PLAN_WARPS * 32, 0,
-                     as_stream(stream)>>>(T.P);
+  launch_pdl(tcp::plan_kernel, dim3((unsigned)ceil_div(T.P.ntile, tcp::PLAN_WARPS)),
+             dim3(tcp::PLAN_WARPS * 32), 0, as_stream(stream), T.P);
   if ((st = check_launch("partial_plan")) != CVB_OK) return st;
   const int64_t grid = T.P.ntile < n_sms ? T.P.ntile : n_sms;
-  tcp::partial_contract_tcp_kernel<<<(unsigned)grid, tcp::THREADS, smem, as_stream(stream)>>>(T);
+  launch_pdl(tcp::partial_contract_tcp_kernel, dim3((unsigned)grid), dim3(tcp::THREADS), smem,
+             as_stream(stream), T);
   if (T.ts != nullptr) {  // debug timeline dump (CTA 0..3, first 64 tiles each), ns
     unsigned long long h[4 * 64 * 8];
     cudaStreamSynchronize(as_stream(stream));
