@@ -283,11 +283,31 @@ __device__ __forceinline__ float pool4f(float a, float b, float c, float d) {
   return __fmul_rn(__fadd_rn(__fadd_rn(a, b), __fadd_rn(c, d)), 0.25f);
 }
 
+__device__ __forceinline__ void split_store(const float (&x)[8], int lane, int kgs,
+                                            int64_t c, int64_t cells, int dp,
+                                            __half* __restrict__ planes,
+                                            int8_t* __restrict__ exps) {
+  const int e = row_exp(x);
+  if (lane < kgs) {
+    uint4 hi, lo;
+    split8(x, exp2_neg(-e), hi, lo);
+    *reinterpret_cast<uint4*>(planes + c * dp + lane * 8) = hi;
+    *reinterpret_cast<uint4*>(planes + cells * dp + c * dp + lane * 8) = lo;
+  }
+  if (lane == 0) exps[c] = (int8_t)e;
+}
+
+// With src_planes, the pooling pass also splits the four source cells of every
+// output cell (the source level is read once); the source cells a 2x2 pool
+// drops (odd trailing row / column) are split by split_tail_kernel.
 __global__ void __launch_bounds__(256) split_level_kernel(const float* __restrict__ src,
                                                           int src_w, float* __restrict__ pooled,
                                                           int h, int w, int d, int dp, bool pool,
                                                           bool vec, __half* __restrict__ planes,
-                                                          int8_t* __restrict__ exps) {
+                                                          int8_t* __restrict__ exps,
+                                                          __half* __restrict__ src_planes,
+                                                          int8_t* __restrict__ src_exps,
+                                                          int64_t src_cells) {
   const int lane = threadIdx.x & 31, kgs = dp / 8;
   const int64_t cells = (int64_t)h * w;
   for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < cells;
@@ -303,6 +323,13 @@ __global__ void __launch_bounds__(256) split_level_kernel(const float* __restric
         load8(r0 + d, d, lane, vec, b);
         load8(r1, d, lane, vec, e);
         load8(r1 + d, d, lane, vec, f);
+        if (src_planes != nullptr) {
+          const int64_t s0 = (int64_t)(2 * y) * src_w + 2 * xx, s1 = s0 + src_w;
+          split_store(a, lane, kgs, s0, src_cells, dp, src_planes, src_exps);
+          split_store(b, lane, kgs, s0 + 1, src_cells, dp, src_planes, src_exps);
+          split_store(e, lane, kgs, s1, src_cells, dp, src_planes, src_exps);
+          split_store(f, lane, kgs, s1 + 1, src_cells, dp, src_planes, src_exps);
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) x[j] = pool4f(a[j], b[j], e[j], f[j]);
         float* o = pooled + c * d;
@@ -325,6 +352,32 @@ __global__ void __launch_bounds__(256) split_level_kernel(const float* __restric
       *reinterpret_cast<uint4*>(planes + cells * dp + c * dp + lane * 8) = lo;
     }
     if (lane == 0) exps[c] = (int8_t)e;
+  }
+}
+
+// Source cells not covered by the 2x2 pool (odd trailing row / column).
+__global__ void __launch_bounds__(256) split_tail_kernel(const float* __restrict__ src, int sh,
+                                                         int sw, int d, int dp, bool vec,
+                                                         __half* __restrict__ planes,
+                                                         int8_t* __restrict__ exps) {
+  const int lane = threadIdx.x & 31, kgs = dp / 8;
+  const int ph = (sh / 2) * 2, pw = (sw / 2) * 2;
+  const int64_t n_rows = (int64_t)(sh - ph) * sw, n = n_rows + (int64_t)ph * (sw - pw);
+  const int64_t cells = (int64_t)sh * sw;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int y, x;
+    if (i < n_rows) {
+      y = ph + (int)(i / sw);
+      x = (int)(i % sw);
+    } else {
+      y = (int)(i - n_rows);
+      x = pw;
+    }
+    const int64_t c = (int64_t)y * sw + x;
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (lane < kgs) load8(src + c * d, d, lane, vec, v);
+    split_store(v, lane, kgs, c, cells, dp, planes, exps);
   }
 }
 
@@ -868,21 +921,38 @@ int cvb_tc_prepare(const cvb_partial_desc* desc, const float* f1, float* const* 
       reinterpret_cast<int8_t*>(f1s + n_tiles * tc::N * dp * 4));
   if ((st = check_launch("tc_split_f1")) != CVB_OK) return st;
   const bool pool = flags & CVB_PREP_POOL;
-  for (int l = 0; l < desc->levels; ++l) {
+  for (int l = 0; l < desc->levels; ++l)
     CVB_REQUIRE(f2_levels_host[l] && f2_split_host[l], "tc_prepare: null level pointer");
+  auto planes_of = [&](int l) { return reinterpret_cast<__half*>(f2_split_host[l]); };
+  auto exps_of = [&](int l) {
+    return reinterpret_cast<int8_t*>(planes_of(l) + 2 * (int64_t)desc->th[l] * desc->tw[l] * dp);
+  };
+  auto aligned = [&](const void* p) { return d % 4 == 0 && ((uintptr_t)p & 15) == 0; };
+  // level 0 is split by the level-1 pooling pass when there is one
+  const bool fuse01 = pool && desc->levels > 1;
+  for (int l = 0; l < desc->levels; ++l) {
     const int h = desc->th[l], w = desc->tw[l];
     const int64_t cells = (int64_t)h * w;
+    if (l == 0 && fuse01) {
+      const int64_t tail = cells - (int64_t)(h / 2) * 2 * ((w / 2) * 2);
+      if (tail > 0) {
+        tc::split_tail_kernel<<<prep_grid(tail), 256, 0, s>>>(
+            f2_levels_host[0], h, w, d, dp, aligned(f2_levels_host[0]), planes_of(0), exps_of(0));
+        if ((st = check_launch("tc_split_tail")) != CVB_OK) return st;
+      }
+      continue;
+    }
     const bool pool_l = pool && l > 0;
     if (pool_l)
       CVB_REQUIRE(desc->th[l - 1] / 2 == h && desc->tw[l - 1] / 2 == w,
                   "tc_prepare: level %d dims are not the 2x2 pool of level %d", l, l - 1);
     const float* src = pool_l ? f2_levels_host[l - 1] : f2_levels_host[l];
-    const bool v = d % 4 == 0 && ((uintptr_t)src & 15) == 0 &&
-                   ((uintptr_t)f2_levels_host[l] & 15) == 0;
-    __half* planes = reinterpret_cast<__half*>(f2_split_host[l]);
+    const bool v = aligned(src) && aligned(f2_levels_host[l]);
+    const bool split_src = fuse01 && l == 1;
     tc::split_level_kernel<<<prep_grid(cells), 256, 0, s>>>(
-        src, pool_l ? desc->tw[l - 1] : w, f2_levels_host[l], h, w, d, dp, pool_l, v, planes,
-        reinterpret_cast<int8_t*>(planes + 2 * cells * dp));
+        src, pool_l ? desc->tw[l - 1] : w, f2_levels_host[l], h, w, d, dp, pool_l, v, planes_of(l),
+        exps_of(l), split_src ? planes_of(0) : nullptr, split_src ? exps_of(0) : nullptr,
+        (int64_t)desc->th[0] * desc->tw[0]);
     if ((st = check_launch("tc_split_level")) != CVB_OK) return st;
   }
   return CVB_OK;

@@ -70,6 +70,16 @@ def test_fused_tc_prepare_pyramid_bit_exact(cuda, shape):
     want = O.pyramid(f2.values.cpu().numpy(), 3)
     for lvl in range(3):
         assert np.array_equal(st.pyramid.levels[lvl].values.cpu().numpy(), want[lvl])
+    # the fused pass (level-0 split inside the level-1 pooling, trailing
+    # row / column separately) writes the same operand bytes as splitting
+    # each level of a precomputed pyramid
+    ref = cvb.init_state(f1, f2, cvb.LookupSpec(4, 3), pyramid=cvb.build_feature_pyramid(f2, 3))
+    dp = -(-d // 64) * 64
+    for lvl, (a, b) in enumerate(zip(st.tc_f2, ref.tc_f2)):
+        cells = int(np.prod(st.pyramid.levels[lvl].values.shape[:2]))
+        n = 4 * cells * dp + cells  # hi + lo planes + exponent bytes (the rest is padding)
+        assert torch.equal(a[:n], b[:n])
+    assert torch.equal(st.tc_f1, ref.tc_f1)
 
 
 def test_floors_and_support_masks_bit_exact(golden, cuda):
