@@ -1,7 +1,7 @@
 # bench each prebuilt library variant in build_variants/*/ (swapped in place)
 cd ${GRAFT_REPO_ROOT:-.}
 cp paper_2505_16942_b200/libcorrvol_b200.so /tmp/lib_orig.so
-for d in build_variants/*/; do
+for d in ${VARDIR:-variants_tmp}/*/; do
   cp $d/libcorrvol_b200.so paper_2505_16942_b200/libcorrvol_b200.so
   timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-compare > gpurun_out/var.json 2>gpurun_out/var.err
   python -c "
