@@ -206,21 +206,23 @@ __device__ __forceinline__ void region_taps(const float* __restrict__ R, const Q
   }
 }
 
+// Pixel of query i of the warp's group: pix0 + (i >> 2) * w1 + (i & 3).
 template <int KK_>
 __device__ __forceinline__ void write_outs(const float* O, unsigned todo, float* out,
-                                           int64_t row0, int levels, int level, int KK,
+                                           int64_t pix0, int w1, int levels, int level, int KK,
                                            int lane) {
   if (KK_ > 0 && todo == 0xFFu) {  // flat loop over the 8 queries' outputs
-    float* base = out + (row0 * levels + level) * (int64_t)KK_;
-    for (int e = lane; e < TQW * KK_; e += 32) {
+    for (int e = lane; e < QG * KK_; e += 32) {
       const int q = e / KK_, t = e - q * KK_;
-      base[(int64_t)q * levels * KK_ + t] = O[e];
+      const int64_t pix = pix0 + (q >> 2) * (int64_t)w1 + (q & 3);
+      out[(pix * levels + level) * (int64_t)KK_ + t] = O[e];
     }
     return;
   }
-  for (int q = 0; q < TQW; ++q) {
+  for (int q = 0; q < QG; ++q) {
     if (!((todo >> q) & 1u)) continue;
-    float* dst = out + ((row0 + q) * levels + level) * (int64_t)KK;
+    const int64_t pix = pix0 + (q >> 2) * (int64_t)w1 + (q & 3);
+    float* dst = out + (pix * levels + level) * (int64_t)KK;
     for (int t = lane; t < KK; t += 32) dst[t] = O[q * KK + t];
   }
 }
@@ -248,9 +250,9 @@ __global__ void __launch_bounds__(WARPS * 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tile = P.tile0 + (blockIdx.x >> 1);
   const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
-  const int qrow = (blockIdx.x & 1) * WARPS + warp;
-  const int py = tile_y * TQH + qrow;
-  if (py >= P.h1) return;  // warp-uniform
+  const int grp = (blockIdx.x & 1) * WARPS + warp;  // query group (2 rows x 4 columns)
+  const int py0 = tile_y * TQH + group_qy(grp, 0), px0 = tile_x * TQW + group_qx(grp, 0);
+  if (py0 >= P.h1) return;  // warp-uniform
 
   const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sm.bar[warp][0]);
   const uint32_t bar1 = (uint32_t)__cvta_generic_to_shared(&sm.bar[warp][1]);
@@ -261,9 +263,9 @@ __global__ void __launch_bounds__(WARPS * 32)
   }
   // ---- centroids once, per-level anchors and weights ----
   bool valid = false;
-  if (lane < TQW) {
-    const int px = tile_x * TQW + lane;
-    valid = px < P.w1;
+  if (lane < QG) {
+    const int py = py0 + (lane >> 2), px = px0 + (lane & 3);
+    valid = py < P.h1 && px < P.w1;
     double x = 0.0, y = 0.0;
     if (valid) load_coord(P.coords, P.f64, (int64_t)py * P.w1 + px, x, y);
     for (int li = 0; li < nlev; ++li) {
@@ -288,13 +290,14 @@ __global__ void __launch_bounds__(WARPS * 32)
   const unsigned vmask = __ballot_sync(0xffffffffu, valid) & 0xFFu;
   __syncwarp();
   if (vmask == 0) return;
-  const int64_t row0 = (int64_t)py * P.w1 + tile_x * TQW;
+  const int64_t pix0 = (int64_t)py0 * P.w1 + px0;
+  auto pix = [&](int q) { return pix0 + (q >> 2) * (int64_t)P.w1 + (q & 3); };
   float* O = sm.outs[warp];
   uint32_t phase0 = 0u, phase1 = 0u;
 
   auto plane_of = [&](int l) {
     const int64_t cap = (int64_t)P.ch[l] * P.cw[l];
-    return P.cache[l] + (tile * TQH + qrow) * cap * TQW;
+    return P.cache[l] + (tile * QG + grp) * cap * QG;
   };
 
   // issue the staged region of level index li into buffer b
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(WARPS * 32)
         }
         region_taps<STRICT, K_>(R, qi, todo, ylo, xlo, rw, r, K, P.scale, P.normalize, O, lane);
         __syncwarp();
-        write_outs<KK_>(O, todo, out, row0, P.levels, l, KK, lane);
+        write_outs<KK_>(O, todo, out, pix0, P.w1, P.levels, l, KK, lane);
         __syncwarp();
         done |= todo;
       }
@@ -352,7 +355,7 @@ __global__ void __launch_bounds__(WARPS * 32)
     const float* f2 = P.f2[l];
     for (int q = 0; q < TQW; ++q) {
       if ((done >> q) & 1u) continue;
-      const float* a = P.f1 + (row0 + q) * d;
+      const float* a = P.f1 + pix(q) * d;
       for (int c = lane; c < S * S; c += 32) {
         const int cy = qi[q].ay - r + c / S, cx = qi[q].ax - r + c % S;
         float v = 0.f;
@@ -381,7 +384,7 @@ __global__ void __launch_bounds__(WARPS * 32)
       }
       __syncwarp();
       emit_patch_taps<STRICT>(R, S, K, qi[q], P.scale, P.normalize,
-                              out + ((row0 + q) * P.levels + l) * (int64_t)KK, lane);
+                              out + (pix(q) * P.levels + l) * (int64_t)KK, lane);
       __syncwarp();
     }
   };
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(WARPS * 32)
       region_taps<STRICT, K_>(sm.region[warp][b], sm.q[warp][li], vmask, g.ylo, g.xlo, g.rw, r,
                               K, P.scale, P.normalize, O, lane);
       __syncwarp();
-      write_outs<KK_>(O, vmask, out, row0, P.levels, level0 + li, KK, lane);
+      write_outs<KK_>(O, vmask, out, pix0, P.w1, P.levels, level0 + li, KK, lane);
       __syncwarp();
     } else {
       slow_level(li, b);

@@ -5,17 +5,18 @@
 // shared-memory region stage: the sampler is bound by instructions and
 // latency, not bytes, when every lane computes staging addresses, so each lane
 // reads exactly the cache sectors its taps need straight into registers.
-//   * one warp per query row of a tile (8 queries), all levels (<= 4 per
-//     launch); lane (q, l) = (lane & 7, lane >> 3) derives the anchor and
-//     weights of query q at level l once (the four levels in parallel);
+//   * one warp per query group of a tile (2 rows x 4 columns = the 8 queries
+//     of one 32-byte cache sector), all levels (<= 4 per launch); lane
+//     (q, l) = (lane & 7, lane >> 3) derives the anchor and weights of query
+//     q at level l once (the four levels in parallel);
 //   * taps: lane (q, l) owns query q at level l: three passes of 3 tap rows,
 //     each loading the 4 x 10 patch values it needs from the cache plane
 //     ([slot][8 queries], 32-byte sectors shared by the row's queries through
 //     L1) into registers, zero outside the level grid, and combining them
 //     (canonical fp32 combine, pre-scaled weights);
-//   * the row's outputs (8 queries x L levels x 81 taps, one contiguous block
-//     of the [H,W,L,9,9] cost map) are staged in shared memory and written with
-//     128-bit stores.
+//   * the group's outputs (two rows of 4 queries x L levels x 81 taps, two
+//     contiguous blocks of the [H,W,L,9,9] cost map) are staged in shared
+//     memory and written with 128-bit stores.
 // Levels whose box overflowed the cache window are evaluated by direct dot
 // products, the warp cooperating on each query's window (gather.cu semantics).
 #include "partial.cuh"
@@ -28,7 +29,7 @@ constexpr int MAXL = 4;    // levels per launch
 constexpr int R = 4, K = 9, KK = 81, S = 10;
 
 struct Shared {
-  float outs[WARPS][TQW * MAXL * KK];  // 10,368 B per warp
+  float outs[WARPS][QG * MAXL * KK];   // 10,368 B per warp
   float patch[WARPS][S * S];           // overflow path: one query's window
 };
 
@@ -37,10 +38,10 @@ struct Shared {
 // the 100 cells, four independent 128-bit-load dot chains per lane — then
 // combines the taps from the staged patch (gather.cu semantics, fmaf dots).
 __device__ __noinline__ void overflow_level(const float* f1, const float* f2, int th, int tw,
-                                            int d, bool vec, int64_t row0, unsigned vmask,
+                                            int d, bool vec, int64_t pix0, int w1, unsigned vmask,
                                             int ay, int ax, Weights32 w, int l_, int nlev,
                                             float* patch, float* O, int lane) {
-  for (int qq = 0; qq < TQW; ++qq) {
+  for (int qq = 0; qq < QG; ++qq) {
     const int src = 8 * l_ + qq;
     const int qay = __shfl_sync(0xffffffffu, ay, src), qax = __shfl_sync(0xffffffffu, ax, src);
     Weights32 qw;
@@ -49,7 +50,7 @@ __device__ __noinline__ void overflow_level(const float* f1, const float* f2, in
     qw.w10 = __shfl_sync(0xffffffffu, w.w10, src);
     qw.w11 = __shfl_sync(0xffffffffu, w.w11, src);
     if (!((vmask >> qq) & 1u)) continue;
-    const float* a = f1 + (row0 + qq) * (int64_t)d;
+    const float* a = f1 + (pix0 + (qq >> 2) * (int64_t)w1 + (qq & 3)) * (int64_t)d;
     const float* b[4];
     bool in[4];
 #pragma unroll
@@ -102,14 +103,14 @@ __global__ void __launch_bounds__(WARPS * 32, 2) gather_fast_kernel(PartialParam
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tile = P.tile0 + blockIdx.x;
   const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
-  const int qrow = warp;
-  const int py = tile_y * TQH + qrow;
-  if (py >= P.h1) return;  // warp-uniform
+  const int grp = warp;  // query group: tile rows 2(g>>1)..+1, columns 4(g&1)..+3
+  const int py0 = tile_y * TQH + group_qy(grp, 0), px0 = tile_x * TQW + group_qx(grp, 0);
+  if (py0 >= P.h1) return;  // warp-uniform
 
   // ---- lane (q, l): anchor, fractions and weights of query q at level l ----
   const int q = lane & 7, li = lane >> 3;
-  const int px = tile_x * TQW + q;
-  const bool qvalid = px < P.w1;
+  const int py = py0 + (q >> 2), px = px0 + (q & 3);
+  const bool qvalid = py < P.h1 && px < P.w1;
   const unsigned vmask = __ballot_sync(0xffffffffu, qvalid) & 0xFFu;
   int ay = 0, ax = 0, status = ST_EMPTY;
   Weights32 w{0.f, 0.f, 0.f, 0.f};
@@ -131,20 +132,20 @@ __global__ void __launch_bounds__(WARPS * 32, 2) gather_fast_kernel(PartialParam
     }
   }
   if (vmask == 0) return;
-  const int64_t row0 = (int64_t)py * P.w1 + tile_x * TQW;
+  const int64_t pix0 = (int64_t)py0 * P.w1 + px0;  // pixel of query i: pix0 + (i>>2)*W + (i&3)
   float* O = sm.outs[warp];  // [q][nlev][81]
   // overflowed levels: warp-cooperative direct dots (warp-uniform loop)
   for (int l_ = 0; l_ < nlev; ++l_) {
     if (__shfl_sync(0xffffffffu, status, 8 * l_) == ST_OVERFLOW)
       overflow_level(P.f1, P.f2[level0 + l_], P.th[level0 + l_], P.tw[level0 + l_], P.d, P.vec,
-                     row0, vmask, ay, ax, w, l_, nlev, sm.patch[warp], O, lane);
+                     pix0, P.w1, vmask, ay, ax, w, l_, nlev, sm.patch[warp], O, lane);
   }
   // every lane (q, l) combines the 81 taps of query q at level l, three tap
   // rows per pass from 4 x 10 cache values loaded into registers
   if (li < nlev && qvalid && status != ST_OVERFLOW) {
     const int l = level0 + li;
     const int th = P.th[l], tw = P.tw[l], ch = P.ch[l], cw = P.cw[l];
-    const float* plane = P.cache[l] + ((tile * TQH + qrow) * (int64_t)(ch * cw)) * TQW + q;
+    const float* plane = P.cache[l] + ((tile * QG + grp) * (int64_t)(ch * cw)) * QG + q;
     const int x0 = ax - R;
     int xs = x0 % cw;
     if (xs < 0) xs += cw;
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) gather_fast_kernel(PartialParam
     bool colin[S];
 #pragma unroll
     for (int i = 0; i < S; ++i) {
-      colofs[i] = xs * TQW;
+      colofs[i] = xs * QG;
       colin[i] = x0 + i >= 0 && x0 + i < tw;
       if (++xs == cw) xs = 0;
     }
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) gather_fast_kernel(PartialParam
       for (int j = 0; j < 4; ++j) {
         const int gy = y0 + j;
         const bool rin = status == ST_OK && gy >= 0 && gy < th;
-        const float* prow = plane + (int64_t)(sy * cw) * TQW;
+        const float* prow = plane + (int64_t)(sy * cw) * QG;
 #pragma unroll
         for (int i = 0; i < S; ++i) v[j][i] = (rin && colin[i]) ? __ldg(prow + colofs[i]) : 0.f;
         if (++sy == ch) sy = 0;
@@ -182,40 +183,44 @@ __global__ void __launch_bounds__(WARPS * 32, 2) gather_fast_kernel(PartialParam
     }
   }
   __syncwarp();
-  // ---- write back ----
+  // ---- write back: the group's two rows of 4 queries ----
   if (P.out_raft) {
     // RAFT CorrBlock layout: out[(l * 81 + dx * 9 + dy) * H * W + pixel]; per
-    // window index the row's 8 queries are 32 contiguous bytes
+    // window index each row of the group is 16 contiguous bytes
     const int64_t hw = (int64_t)P.h1 * P.w1;
-    const bool vec4 = vmask == 0xFFu && (row0 & 3) == 0 && (hw & 3) == 0 &&
-                      ((uintptr_t)out & 15) == 0;
     for (int e = lane; e < nlev * KK * 2; e += 32) {
       const int hq = e & 1, lt = e >> 1;
       const int l_ = lt / KK, t = lt - l_ * KK;
       const int dy = t / K, dx = t - dy * K;
-      float* dst = out + ((int64_t)(level0 + l_) * KK + dx * K + dy) * hw + row0 + 4 * hq;
+      const unsigned rowmask = (vmask >> (4 * hq)) & 0xFu;
+      float* dst = out + ((int64_t)(level0 + l_) * KK + dx * K + dy) * hw + pix0 + hq * P.w1;
       const float* src = O + (4 * hq) * nlev * KK + lt;
-      if (vec4) {
+      if (rowmask == 0xFu && (((uintptr_t)dst) & 15) == 0) {
         *reinterpret_cast<float4*>(dst) =
             make_float4(src[0], src[nlev * KK], src[2 * nlev * KK], src[3 * nlev * KK]);
       } else {
         for (int k = 0; k < 4; ++k)
-          if ((vmask >> (4 * hq + k)) & 1u) dst[k] = src[k * nlev * KK];
+          if ((rowmask >> k) & 1u) dst[k] = src[k * nlev * KK];
       }
     }
-  } else if (nlev == P.levels && vmask == 0xFFu && (P.levels * KK) % 4 == 0 &&
-      ((uintptr_t)out & 15) == 0) {
-    // one contiguous 16-byte-aligned block of 8 * L * 81 floats
-    const int n4 = TQW * nlev * KK / 4;
-    float4* dst = reinterpret_cast<float4*>(out + row0 * (int64_t)(P.levels * KK));
-    const float4* src4 = reinterpret_cast<const float4*>(O);
-    for (int i = lane; i < n4; i += 32) dst[i] = src4[i];
   } else {
-    for (int qq = 0; qq < TQW; ++qq) {
-      if (!((vmask >> qq) & 1u)) continue;
-      for (int e = lane; e < nlev * KK; e += 32) {
-        const int l_ = e / KK, t = e - l_ * KK;
-        out[((row0 + qq) * P.levels + level0 + l_) * (int64_t)KK + t] = O[(qq * nlev + l_) * KK + t];
+    for (int hq = 0; hq < 2; ++hq) {
+      const unsigned rowmask = (vmask >> (4 * hq)) & 0xFu;
+      const float* src = O + 4 * hq * nlev * KK;
+      float* dst = out + (pix0 + hq * P.w1) * (int64_t)(P.levels * KK);
+      if (rowmask == 0xFu && nlev == P.levels && (((uintptr_t)dst) & 15) == 0) {
+        // 4 consecutive pixels x L x 81 floats: one contiguous block
+        const int n4 = 4 * nlev * KK / 4;
+        for (int i = lane; i < n4; i += 32)
+          reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
+      } else {
+        for (int k = 0; k < 4; ++k) {
+          if (!((rowmask >> k) & 1u)) continue;
+          for (int e = lane; e < nlev * KK; e += 32) {
+            const int l_ = e / KK, t = e - l_ * KK;
+            dst[(int64_t)k * P.levels * KK + (level0 + l_) * KK + t] = src[k * nlev * KK + e];
+          }
+        }
       }
     }
   }

@@ -79,9 +79,12 @@ __global__ void __launch_bounds__(GEMM_THREADS) partial_contract_kernel(PartialP
       int cy, cx;
       new_cell(B, I, has_i, idx, cy, cx);
       float4 v = make_float4(acc[0][j], acc[1][j], acc[2][j], acc[3][j]);
-      // cache layout [query row][slot][8 queries]; queries ty*4..ty*4+3
+      // queries ty*4..ty*4+3: tile row ty>>1, columns (ty&1)*4..+3 -> one
+      // group, 4 consecutive group indices (cache layout [group][slot][8])
+      const int qy = ty >> 1, qx0 = (ty & 1) * 4;
       *reinterpret_cast<float4*>(
-          cache + ((int64_t)(ty >> 1) * (ch * cw) + slot_of(cy, cx, ch, cw)) * TQW + (ty & 1) * 4) = v;
+          cache + ((int64_t)qgroup(qy, qx0) * (ch * cw) + slot_of(cy, cx, ch, cw)) * QG +
+          qindex(qy, qx0)) = v;
     }
   }
 }

@@ -721,7 +721,9 @@ __global__ void __launch_bounds__(THREADS, 1)
               o.y = fmaf(vc[j + 1], 1.f / (1 << tc::LOG2_LO), vm[j + 1]) * (s_q[q + 1] * s_c);
               o.z = fmaf(vc[j + 2], 1.f / (1 << tc::LOG2_LO), vm[j + 2]) * (s_q[q + 2] * s_c);
               o.w = fmaf(vc[j + 3], 1.f / (1 << tc::LOG2_LO), vm[j + 3]) * (s_q[q + 3] * s_c);
-              *reinterpret_cast<float4*>(dst + (q >> 3) * plane + (q & 7)) = o;
+              // queries q..q+3 share tile row q>>3: one group, 4 consecutive slots
+              *reinterpret_cast<float4*>(dst + qgroup(q >> 3, q & 7) * plane +
+                                         qindex(q >> 3, q & 7)) = o;
             }
           }
         }
