@@ -692,20 +692,23 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       for (int c = 0; c < n_chunks; ++c, ++cg) {
         const int ab = cg & 1;
-        wait_full(U(C.acc_full[ab]), cg >> 1);
-        tc::tc_fence_after();
+        // the row's cell, cache slot and exponent depend only on the plan:
+        // resolve them (and issue the exponent load) before the accumulator wait
         const int gi = c * tc::M + ep;
         float* dst = nullptr;
         int64_t plane = 0;
-        float s_c = 0.f;
+        int e_c = 0;
         if (gi < n) {
           const tc::CellRef cr = tc::cell_of(gi, S.plan, S.prefix, P.levels);
           const int ch = P.ch[cr.level], cw = P.cw[cr.level];
           plane = (int64_t)ch * cw * TQW;
           dst = P.cache[cr.level] + tile * plane * TQH +
                 (int64_t)slot_of(cr.cy, cr.cx, ch, cw) * TQW;
-          s_c = tc::exp2_neg(T.e2[cr.level][(int64_t)cr.cy * P.tw[cr.level] + cr.cx]);
+          e_c = T.e2[cr.level][(int64_t)cr.cy * P.tw[cr.level] + cr.cx];
         }
+        wait_full(U(C.acc_full[ab]), cg >> 1);
+        tc::tc_fence_after();
+        const float s_c = tc::exp2_neg(e_c);
         float vm[32], vc[32];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
