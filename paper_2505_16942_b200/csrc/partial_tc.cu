@@ -563,6 +563,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int ab = cg & 1;
             wait_empty(U(C.acc_empty[ab]), cg >> 1);
             tc::tc_fence_after();
+            if (c == 0) stamp(T, it, 6);
             const uint32_t d_main = tmem + ab * 128, d_corr = d_main + 64;
             for (int kb = 0; kb < n_kb; ++kb, ++g) {
               const uint32_t pi = pb + kb;
@@ -571,6 +572,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               const int st = (int)(g % NST);
               wait_full(U(C.a_full[st]), g / NST);
               tc::tc_fence_after();
+              if (c == 0 && kb == 0) stamp(T, it, 7);
               const uint32_t a_hi = uA + st * tc::A_STAGE, a_lo = a_hi + tc::A_HALF;
               const uint32_t b_hi = uB + bs * tc::B_PIECE, b_lo = b_hi + tc::B_HALF;
               if (!(T.dbg & 4)) {
@@ -1030,9 +1032,10 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
       for (int it = 0; it < 64; ++it) {
         const unsigned long long* e = h + (b * 64 + it) * 8;
         if (e[1] == 0) break;
-        fprintf(stderr, "TS call %d cta %d it %2d plan %7.2f mma0 %7.2f mma1 %7.2f A %7.2f epi %7.2f B %7.2f\n",
+        fprintf(stderr, "TS call %d cta %d it %2d plan %7.2f mma0 %7.2f mma1 %7.2f A %7.2f epi %7.2f B %7.2f accE %7.2f a0 %7.2f\n",
                 call, b, it, (e[0] - t0) * 1e-3, (e[1] - t0) * 1e-3, (e[2] - t0) * 1e-3,
-                (e[3] - t0) * 1e-3, (e[4] - t0) * 1e-3, (e[5] - t0) * 1e-3);
+                (e[3] - t0) * 1e-3, (e[4] - t0) * 1e-3, (e[5] - t0) * 1e-3, (e[6] - t0) * 1e-3,
+                (e[7] - t0) * 1e-3);
       }
   }
   return check_launch("partial_contract_tcp");
