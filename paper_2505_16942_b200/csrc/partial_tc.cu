@@ -9,10 +9,11 @@
 //   * split precision: every fp32 value x (pre-scaled by a per-tensor power of
 //     two so it sits in fp16 range) is stored as hi = fp16(x) and
 //     lo = fp16((x - hi) * 2^11); x*y = hi_x*hi_y + 2^-11 (hi_x*lo_y + lo_x*hi_y)
-//     + O(2^-22).  Three MMAs per K-step (main += hi.hi; corr += hi.lo;
-//     corr += lo.hi) keep ~22 significant bits per product at 2x the TF32
-//     tensor rate, well inside the fp32 tolerance (products of two fp16 are
-//     exact in the fp32 accumulator);
+//     + O(2^-22).  Per K-step one N=128 MMA (the F1 piece's hi and lo rows
+//     form one 128-row B matrix: main += hi.hi and corr += hi.lo, reading
+//     A_hi from shared memory once) and one N=64 MMA (corr += lo.hi) keep ~22
+//     significant bits per product (products of two fp16 are exact in the
+//     fp32 accumulator);
 //   * operands are pre-split once per image pair (cvb_tc_prepare): the F1
 //     tile is a contiguous image of its shared-memory layout cut into K
 //     pieces of 64 channels (16 KB: hi 8 KB + lo 8 KB), each fetched with one
@@ -47,6 +48,11 @@ constexpr int TARGET_EXP = 14;           // max |x * 2^e| < 2^14
 
 // instruction descriptor: D f32, A/B f16, both K-major, N=64, M=128
 constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// N = 2 x 64: the F1 piece's hi and lo halves form one 128-row B matrix, so
+// main (A_hi . B_hi) and the first correction (A_hi . B_lo) are one MMA that
+// reads A_hi from shared memory once (the MMA phase is smem-read-bound)
+constexpr uint32_t IDESC_N128 =
+    (1u << 4) | ((uint32_t)(2 * N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -77,12 +83,13 @@ __device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr) {
   return d;
 }
 
+template <uint32_t ID = IDESC>
 __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+      "l"(a), "l"(b), "r"(ID), "r"(acc));
 }
 
 __device__ __forceinline__ void mma_commit(uint32_t mbar) {
@@ -574,18 +581,17 @@ __global__ void __launch_bounds__(THREADS, 1)
               tc::tc_fence_after();
               if (c == 0 && kb == 0) stamp(T, it, 7);
               const uint32_t a_hi = uA + st * tc::A_STAGE, a_lo = a_hi + tc::A_HALF;
-              const uint32_t b_hi = uB + bs * tc::B_PIECE, b_lo = b_hi + tc::B_HALF;
+              const uint32_t b_hi = uB + bs * tc::B_PIECE;  // hi rows 0-63, lo rows 64-127
               if (!(T.dbg & 4)) {
 #pragma unroll
                 for (int k = 0; k < tc::KP / 16; ++k) {
                   const uint64_t dah = tc::make_desc_sw128(a_hi + k * 32);
                   const uint64_t dal = tc::make_desc_sw128(a_lo + k * 32);
                   const uint64_t dbh = tc::make_desc(b_hi + k * 256, 128, (tc::KP / 8) * 128);
-                  const uint64_t dbl = tc::make_desc(b_lo + k * 256, 128, (tc::KP / 8) * 128);
-                  const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-                  tc::mma_f16(d_main, dah, dbh, acc);
-                  tc::mma_f16(d_corr, dah, dbl, acc);
-                  tc::mma_f16(d_corr, dal, dbh, 1u);
+                    const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+                  // cols 0-63 += A_hi B_hi (main), cols 64-127 += A_hi B_lo (corr)
+                  tc::mma_f16<tc::IDESC_N128>(d_main, dah, dbh, acc);
+                  tc::mma_f16(d_corr, dal, dbh, 1u);  // corr += A_lo B_hi
                 }
               }
               tc::mma_commit(U(C.a_empty[st]));
