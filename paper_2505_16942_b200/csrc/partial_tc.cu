@@ -128,6 +128,11 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       : "memory");
 }
 
+__device__ __forceinline__ void st_global_v8(float* p, const float (&v)[8]) {
+  asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]),
+               "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -723,18 +728,24 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc::tmem_ld32(tmem + ab * 128 + lane_base + h * 32, vm);
           tc::tmem_ld32(tmem + ab * 128 + 64 + lane_base + h * 32, vc);
           if (dst != nullptr && !(T.dbg & 2)) {
+            // this half holds tile rows 4h..4h+3 = query groups 4h/2*2 .. +3;
+            // each group's 8 costs (32 B, one cache sector) leave in one
+            // 256-bit store, so a warp writes whole sectors of consecutive slots
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const int q = h * 32 + j;
-              float4 o;
-              // (main + 2^-11 corr) * 2^-(e_q + e_c): exact power-of-two scales
-              o.x = fmaf(vc[j + 0], 1.f / (1 << tc::LOG2_LO), vm[j + 0]) * (s_q[q + 0] * s_c);
-              o.y = fmaf(vc[j + 1], 1.f / (1 << tc::LOG2_LO), vm[j + 1]) * (s_q[q + 1] * s_c);
-              o.z = fmaf(vc[j + 2], 1.f / (1 << tc::LOG2_LO), vm[j + 2]) * (s_q[q + 2] * s_c);
-              o.w = fmaf(vc[j + 3], 1.f / (1 << tc::LOG2_LO), vm[j + 3]) * (s_q[q + 3] * s_c);
-              // queries q..q+3 share tile row q>>3: one group, 4 consecutive slots
-              *reinterpret_cast<float4*>(dst + qgroup(q >> 3, q & 7) * plane +
-                                         qindex(q >> 3, q & 7)) = o;
+            for (int gg = 0; gg < 4; ++gg) {
+              const int r = gg >> 1, c = gg & 1;  // row pair and column half in this half
+              const int j0 = 16 * r + 4 * c, j1 = j0 + 8;
+              float o[8];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                // (main + 2^-11 corr) * 2^-(e_q + e_c): exact power-of-two scales
+                o[i] = fmaf(vc[j0 + i], 1.f / (1 << tc::LOG2_LO), vm[j0 + i]) *
+                       (s_q[h * 32 + j0 + i] * s_c);
+                o[4 + i] = fmaf(vc[j1 + i], 1.f / (1 << tc::LOG2_LO), vm[j1 + i]) *
+                           (s_q[h * 32 + j1 + i] * s_c);
+              }
+              const int g = (2 * h + r) * 2 + c;  // == qgroup(4h + 2r, 4c)
+              tc::st_global_v8(dst + g * plane, o);
             }
           }
         }
