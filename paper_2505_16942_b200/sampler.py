@@ -33,7 +33,7 @@ class CorrSampler:
     def __init__(self, fmap1, fmap2, spec: LookupSpec, variant: str = "partial", block: int = 8,
                  cache: bool = True, strict: bool = False, mode: str = "tile",
                  dense_mode: str = "pool_features", dense_limit_bytes: Optional[int] = None,
-                 check: bool = True, **state_kwargs):
+                 check: bool = True, graph: bool = False, **state_kwargs):
         variant = _ALIASES.get(variant, variant)
         if variant not in VARIANTS:
             raise ValueError(f"variant must be one of {VARIANTS}, got {variant!r}")
@@ -43,6 +43,15 @@ class CorrSampler:
         self.f1 = fmap1 if isinstance(fmap1, FeatureMap) else FeatureMap(fmap1, check=check)
         self.f2 = fmap2 if isinstance(fmap2, FeatureMap) else FeatureMap(fmap2, check=check)
         self.check = check
+        # graph=True (partial variant): after one eager call, each iteration's
+        # launch sequence (tiler, contraction, sampler) is replayed from a
+        # captured CUDA graph on static coordinate / output buffers — for
+        # launch-bound frames; the returned tensor is reused by the next call
+        self.graph = graph and variant == "partial"
+        self._graph = None
+        self._g_coords = None
+        self._g_out = None
+        self._eager_calls = 0
         self.state = None
         self.volume = None
         self.pyramid = None
@@ -68,11 +77,43 @@ class CorrSampler:
         cents = coords if isinstance(coords, CentroidField) else CentroidField(coords,
                                                                                 check=self.check)
         if self.variant == "partial":
+            if self.graph:
+                return self._graphed(cents, out)
             return sample_iteration(self.state, cents, out=out)
         if self.variant == "ondemand":
             return lookup_on_demand(self.f1, self.pyramid, cents, self.spec, strict=self.strict,
                                     out=out)
         return lookup_dense(self.volume, cents, self.spec, strict=self.strict, out=out)
+
+    def _graphed(self, cents: CentroidField, out: Optional[torch.Tensor]) -> CostMaps:
+        c = cents.coords
+        if self._graph is None:
+            if self._eager_calls == 0:  # first call eagerly: library setup, iteration 0
+                self._eager_calls += 1
+                return sample_iteration(self.state, cents, out=out)
+            self._g_coords = torch.empty_like(c)
+            self._g_coords.copy_(c)
+            k = self.spec.window
+            self._g_out = torch.empty((self.f1.height, self.f1.width, self.spec.levels, k, k),
+                                      dtype=torch.float32, device=c.device)
+            g_cents = CentroidField(self._g_coords, check=False)
+            torch.cuda.synchronize(c.device)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                sample_iteration(self.state, g_cents, out=self._g_out)
+            self.state.iteration -= 1  # capture recorded the launches without running them
+            self._graph = graph
+        elif c.shape != self._g_coords.shape or c.dtype != self._g_coords.dtype:
+            raise ValueError("graph mode needs coords of the captured shape and dtype")
+        else:
+            self._g_coords.copy_(c)
+        self._graph.replay()
+        self.state.iteration += 1
+        res = self._g_out
+        if out is not None:
+            out.copy_(res)
+            res = out
+        return CostMaps(values=res, radius=self.spec.radius)
 
     def memory_bytes(self) -> int:
         """Analytic bytes the variant holds between iterations."""

@@ -425,3 +425,19 @@ def test_batch_sampler_equals_per_pair(cuda):
         got = batch(coords).cpu().numpy()
         for i in range(3):
             assert np.array_equal(got[i], singles[i](cvb.CentroidField(coords[i])).numpy())
+
+
+def test_graph_mode_equals_eager(cuda):
+    """CorrSampler(graph=True) replays captured iterations: same results."""
+    spec = cvb.LookupSpec(4, 4)
+    sc = cvb.gen_scenario(8, (46, 62, 64), 5, spec, coords_dtype=np.float32)
+    f1 = cvb.FeatureMap(torch.from_numpy(sc.f1).to(cuda))
+    f2 = cvb.FeatureMap(torch.from_numpy(sc.f2).to(cuda))
+    eager = cvb.CorrSampler(f1, f2, spec)
+    graphed = cvb.CorrSampler(f1, f2, spec, graph=True)
+    for c in sc.centroid_fields:
+        ct = torch.from_numpy(c).to(cuda)
+        want = eager(cvb.CentroidField(ct)).values.clone()
+        got = graphed(cvb.CentroidField(ct)).values
+        assert torch.equal(got, want)
+    assert graphed._graph is not None and graphed.state.iteration == 5
