@@ -1,8 +1,11 @@
-// (5) Gather / bilinear sampler of the partial path, reading the tile cache.
+// (5) Gather / bilinear sampler of the partial path, reading the tile cache:
+// the reference-exact (strict, fp64 combine) sampler and the fast sampler for
+// radii other than 4 (fast r=4 is gather_fast.cu).
 //
-// One warp per query row of a tile (8 queries) handles ALL levels, so the
-// centroids are read once and the levels pipeline: while level l's taps are
-// combined, level l+1's cache region is already in flight.
+// One warp per query group of a tile (2 rows x 4 columns, the 8 queries of a
+// cache sector) handles ALL levels, so the centroids are read once and the
+// levels pipeline: while level l's taps are combined, level l+1's cache region
+// is already in flight.
 //   * staging: the union of the 8 supports of a level is a rectangle of
 //     cells; in the warp's cache plane ([slot][8 queries], 32 B per cell)
 //     every in-grid row of it is one contiguous run of slots (two if it wraps
@@ -12,10 +15,10 @@
 //   * taps: one (query, tap row) per lane-iteration; the two region rows a tap
 //     row needs are read once and combined in registers with the canonical
 //     association (fp64 in strict mode, _pykernels.py:99-115); the radius is a
-//     template constant for r=4 (RAFT / SEA-RAFT) so the loops unroll;
+//     template constant for strict r=4 so the loops unroll;
 //   * outputs are staged per level in shared memory and written per query as
 //     81 contiguous floats.
-// Rows whose 8 supports do not fit one region (divergent flow) are processed
+// Groups whose 8 supports do not fit one region (divergent flow) are processed
 // as two groups of 4, then per query; tiles whose box overflowed the cache
 // window are evaluated directly (dot products) — all bit-identical in strict
 // mode.
@@ -34,8 +37,7 @@ constexpr int MAX_TAPS = 81;     // r <= 4 for the staged-output path
 struct QInfo {
   int ay, ax;
   double fx, fy;
-  Weights32 w32;   // fp32 weights (fallback path applies the scale separately)
-  Weights32 w32s;  // fp32 weights pre-multiplied by the 1/sqrt(D) scale (fast path)
+  Weights32 w32;   // fp32 weights (the 1/sqrt(D) scale is applied after the combine)
 };
 
 struct Shared {
@@ -134,44 +136,12 @@ __device__ __forceinline__ bool stage_region(float* R, uint32_t bar, const float
   return true;
 }
 
-// Fast-arithmetic taps for r=4 (K=9): lane (q, g) computes tap rows 3g..3g+2
-// of query q from 4 region rows held in registers (40 shared loads, 27 taps).
-__device__ __forceinline__ void region_taps_r4(const float* __restrict__ R, const QInfo* qi,
-                                               unsigned todo, int ylo, int xlo, int rw,
-                                               float* __restrict__ O, int lane) {
-  constexpr int K = 9, KK = 81, r = 4;
-  if (lane >= 24) return;
-  const int q = lane & 7, g = lane >> 3;
-  if (!((todo >> q) & 1u)) return;
-  const float* a = R + ((qi[q].ay - r - ylo + 3 * g) * rw + (qi[q].ax - r - xlo)) * TQW + q;
-  const Weights32 w = qi[q].w32s;
-  float* o = O + q * KK + 3 * g * K;
-  float r0[K + 1], r1[K + 1];
-#pragma unroll
-  for (int i = 0; i <= K; ++i) r0[i] = a[i * TQW];
-#pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    const float* b = a + (j + 1) * rw * TQW;
-#pragma unroll
-    for (int i = 0; i <= K; ++i) r1[i] = b[i * TQW];
-#pragma unroll
-    for (int i = 0; i < K; ++i)
-      o[j * K + i] = combine32(r0[i], r0[i + 1], r1[i], r1[i + 1], w);
-#pragma unroll
-    for (int i = 0; i <= K; ++i) r0[i] = r1[i];
-  }
-}
-
 // Taps of the queries in `todo` from a staged region into outs[q][K*K].
 template <bool STRICT, int K_>
 __device__ __forceinline__ void region_taps(const float* __restrict__ R, const QInfo* qi,
                                             unsigned todo, int ylo, int xlo, int rw, int r, int K,
                                             float scale, bool normalize, float* __restrict__ O,
                                             int lane) {
-  if (!STRICT && K_ == 9) {
-    region_taps_r4(R, qi, todo, ylo, xlo, rw, O, lane);
-    return;
-  }
   const int KK = K * K;
   for (int e = lane; e < TQW * K; e += 32) {
     const int q = e & (TQW - 1), dy = e >> 3;
@@ -270,7 +240,7 @@ __global__ void __launch_bounds__(WARPS * 32)
     if (valid) load_coord(P.coords, P.f64, (int64_t)py * P.w1 + px, x, y);
     for (int li = 0; li < nlev; ++li) {
       const int l = level0 + li;
-      QInfo qi{0, 0, 0.0, 0.0, Weights32{0.f, 0.f, 0.f, 0.f}, Weights32{0.f, 0.f, 0.f, 0.f}};
+      QInfo qi{0, 0, 0.0, 0.0, Weights32{0.f, 0.f, 0.f, 0.f}};
       if (valid) {
         const LevelPos lp = level_pos(x, y, l);
         qi.ay = clamp_anchor(lp.y0, r, P.th[l]);
@@ -278,8 +248,6 @@ __global__ void __launch_bounds__(WARPS * 32)
         qi.fx = lp.fx;
         qi.fy = lp.fy;
         qi.w32 = weights32(lp.fx, lp.fy);
-        const float sc = P.normalize ? P.scale : 1.0f;
-        qi.w32s = Weights32{qi.w32.w00 * sc, qi.w32.w01 * sc, qi.w32.w10 * sc, qi.w32.w11 * sc};
       }
       sm.q[warp][li][lane] = qi;
     }
@@ -435,26 +403,17 @@ static void launch_one(const PartialParams& P, float* out, int l0, int nl, cudaS
 }
 
 int launch_gather_kernel(const PartialParams& P, float* out, bool strict, cudaStream_t s) {
-  static int fast = -1;
-  if (fast < 0) {
-    const char* e = getenv("CVB_GATHER_FAST");
-    fast = (e == nullptr || e[0] != '0') ? 1 : 0;
-  }
-  if (!strict && P.radius == 4 && (fast || P.out_raft)) return launch_gather_fast_r4(P, out, s);
+  // fast arithmetic at r=4 (RAFT / SEA-RAFT): the register-direct sampler
+  if (!strict && P.radius == 4) return launch_gather_fast_r4(P, out, s);
   CVB_REQUIRE(!P.out_raft, "CVB_OUT_RAFT needs the fast-arithmetic r=4 sampler");
   for (int l0 = 0; l0 < P.levels; l0 += gather::MAXL) {
     const int nl = min(gather::MAXL, P.levels - l0);
-    if (P.radius == 4) {
-      if (strict)
-        launch_one<true, 4>(P, out, l0, nl, s);
-      else
-        launch_one<false, 4>(P, out, l0, nl, s);
-    } else {
-      if (strict)
-        launch_one<true, -1>(P, out, l0, nl, s);
-      else
-        launch_one<false, -1>(P, out, l0, nl, s);
-    }
+    if (strict && P.radius == 4)
+      launch_one<true, 4>(P, out, l0, nl, s);
+    else if (strict)
+      launch_one<true, -1>(P, out, l0, nl, s);
+    else
+      launch_one<false, -1>(P, out, l0, nl, s);
     const int st = check_launch("partial_gather");
     if (st != CVB_OK) return st;
   }
