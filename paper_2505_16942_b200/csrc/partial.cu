@@ -102,7 +102,8 @@ int cvb_partial_sizes(const cvb_partial_desc* desc, int64_t* n_tiles, int64_t* m
   const int64_t nt = ceil_div(desc->h1, TQH) * ceil_div(desc->w1, TQW);
   if (n_tiles) *n_tiles = nt;
   // per-level metadata, then one plan record per tile (tensor-core path)
-  if (meta_ints) *meta_ints = nt * desc->levels * CVB_META_INTS + nt * PLAN_INTS;
+  // (plus one record's worth of ints for the contraction's tile counter)
+  if (meta_ints) *meta_ints = nt * desc->levels * CVB_META_INTS + (nt + 1) * PLAN_INTS;
   if (cache_floats_per_level)
     for (int l = 0; l < desc->levels; ++l)
       cache_floats_per_level[l] = nt * (int64_t)desc->cap_h[l] * desc->cap_w[l] * TQ;

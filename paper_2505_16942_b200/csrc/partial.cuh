@@ -100,7 +100,8 @@ struct alignas(16) PlanRec {
   TilePlan plan[CVB_MAX_LEVELS];
   int prefix[CVB_MAX_LEVELS + 1];  // cells of levels < l in the tile's new-cell list
   int n_cells;
-  int pad[2];
+  int tile;    // the record's tile (-1: end of the work list)
+  int pad;
 };
 constexpr int PLAN_INTS = (int)(sizeof(PlanRec) / 4);
 

@@ -475,6 +475,13 @@ __device__ __forceinline__ void arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+// Work counter of the persistent contraction: the plan loader of every CTA
+// claims the next tile with one atomicAdd (dynamic load balance); it lives in
+// the spare record after the n_tiles plan records and is reset by plan_kernel.
+__device__ __forceinline__ int* tile_counter(const PartialParams& P) {
+  return P.plans + P.n_tiles * PLAN_INTS;
+}
+
 __device__ __forceinline__ void stamp(const tc::TcParams& T, int64_t it, int e) {
   if (T.ts != nullptr && blockIdx.x < 4 && it < 64) {
     unsigned long long t;
@@ -536,12 +543,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       uint32_t pb = 0;  // pieces issued so far
       for (int64_t it = 0;; ++it) {
-        const int64_t t = blockIdx.x + it * gridDim.x;
-        if (t >= P.ntile) break;
         const int s = (int)(it % NPL);
         wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
+        const int tile_i = C.slot[s].tile;
+        if (tile_i < 0) break;
         if (C.slot[s].n_cells > 0) {
-          const uint8_t* src = T.f1s + (P.tile0 + t) * (int64_t)n_kb * tc::B_PIECE;
+          const uint8_t* src = T.f1s + (int64_t)tile_i * n_kb * tc::B_PIECE;
           for (int q = 0; q < n_kb; ++q, ++pb) {
             const int bs = (int)(pb % NBP);
             wait_empty(U(C.b_empty[bs]), pb / NBP);
@@ -563,10 +570,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       uint32_t pb = 0, g = 0, cg = 0;
       for (int64_t it = 0;; ++it) {
-        const int64_t t = blockIdx.x + it * gridDim.x;
-        if (t >= P.ntile) break;
         const int s = (int)(it % NPL);
         wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
+        if (C.slot[s].tile < 0) break;
         stamp(T, it, 1);
         const int n = C.slot[s].n_cells;
         if (n > 0) {
@@ -614,10 +620,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------- plan loader: one bulk copy per tile record ----------------
     if (lane == 0) {
       for (int64_t it = 0;; ++it) {
-        const int64_t t = blockIdx.x + it * gridDim.x;
-        if (t >= P.ntile) break;
         const int s = (int)(it % NPL);
         wait_empty(U(C.plan_empty[s]), (uint32_t)(it / NPL));
+        const int64_t t = atomicAdd(tile_counter(P), 1);  // dynamic tile scheduler
+        if (t >= P.ntile) {  // end of the work list: a sentinel record
+          C.slot[s].tile = -1;
+          arrive(U(C.plan_full[s]));
+          break;
+        }
         tc::mbar_expect_tx(U(C.plan_full[s]), (uint32_t)sizeof(PlanRec));
         tc::bulk_g2s(tc::smem_u32(&C.slot[s]), P.plans + (P.tile0 + t) * PLAN_INTS,
                      (uint32_t)sizeof(PlanRec), U(C.plan_full[s]));
@@ -635,11 +645,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int sub = lane >> 3, chunk = lane & 7;
     uint32_t g = 0;  // A stages issued
     for (int64_t it = 0;; ++it) {
-      const int64_t t = blockIdx.x + it * gridDim.x;
-      if (t >= P.ntile) break;
       const int s = (int)(it % NPL);
       wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
       const PlanRec& S = C.slot[s];
+      if (S.tile < 0) break;
       const int n = S.n_cells;
       const int n_chunks = (n + tc::M - 1) / tc::M;
       for (int c = 0; c < n_chunks; ++c) {
@@ -689,12 +698,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     float* s_q = reinterpret_cast<float*>(&C.qscale[0]);
     uint32_t cg = 0;
     for (int64_t it = 0;; ++it) {
-      const int64_t t = blockIdx.x + it * gridDim.x;
-      if (t >= P.ntile) break;
-      const int64_t tile = P.tile0 + t;
       const int s = (int)(it % NPL);
       wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
       const PlanRec& S = C.slot[s];
+      if (S.tile < 0) break;
+      const int64_t tile = S.tile;
       const int n = S.n_cells;
       const int n_chunks = (n + tc::M - 1) / tc::M;
       if (n_chunks > 0) {
@@ -771,6 +779,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 // per-level meta; the work counters are reduced per CTA (one atomic each).
 constexpr int PLAN_WARPS = 8;
 
+
 __global__ void __launch_bounds__(PLAN_WARPS * 32) plan_kernel(PartialParams P) {
   __shared__ unsigned long long s_cnt[4];
   pdl_trigger();
@@ -778,6 +787,7 @@ __global__ void __launch_bounds__(PLAN_WARPS * 32) plan_kernel(PartialParams P) 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0ULL;
   __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *tile_counter(P) = 0;  // scheduler reset
   const int64_t t = (int64_t)blockIdx.x * PLAN_WARPS + warp;
   if (t < P.ntile) {
     const int64_t tile = P.tile0 + t;
@@ -871,6 +881,7 @@ __global__ void __launch_bounds__(PLAN_WARPS * 32) plan_kernel(PartialParams P) 
     int* prefix = rec + CVB_MAX_LEVELS * (int)(sizeof(TilePlan) / 4);
     if (lane <= P.levels) prefix[lane] = pre - n_new;       // exclusive prefix, lanes 0..L
     if (lane == P.levels) prefix[CVB_MAX_LEVELS + 1] = pre - n_new;  // n_cells
+    if (lane == 0) prefix[CVB_MAX_LEVELS + 2] = (int)tile;           // the record's tile
     unsigned long long c_dots = (unsigned long long)n_new * nv, c_cells = n_new;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

@@ -69,7 +69,7 @@ def test_partial_sizes_host_only():
     _lib.call("cvb_partial_sizes", C.byref(d), C.byref(nt), C.byref(mi), per)
     assert nt.value == 68 * 120
     # per-level meta (8 ints per tile and level) + one 108-int plan record per tile
-    assert mi.value == nt.value * 4 * 8 + nt.value * 108
+    assert mi.value == nt.value * 4 * 8 + (nt.value + 1) * 108
     assert per[0] == nt.value * 24 * 24 * 64
     f1b = C.c_int64()
     _lib.call("cvb_tc_sizes", C.byref(d), C.byref(f1b), per)
