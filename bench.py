@@ -426,6 +426,14 @@ def main():
                      "executed_flops": executed,
                      "note": "achieved = algorithmic flops (2*D*compulsory union cells, "
                              "profiles/geometry_*.json) / measured contraction time"}
+        # measured DRAM traffic of one warm launch (committed ncu capture) over
+        # the warm launch time: how close each kernel runs to the HBM roofline
+        for r_, warm_ms in ((r_gather, statistics.mean(kern["gather_ms"][1:])),
+                            (r_con, statistics.mean(kern["contract_ms"][1:]))):
+            if r_ is not None and r_.get("traffic"):
+                gbs = r_["traffic"] / (warm_ms / 1e3) / 1e9
+                r_["traffic_gbs_warm"] = round(gbs, 1)
+                r_["traffic_frac_of_hbm_peak"] = round(gbs / hbm_peak, 4)
         if r_con is not None and tc >= tg:
             roofline, secondary = r_con, r_gather
         else:
