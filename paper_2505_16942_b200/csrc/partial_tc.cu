@@ -486,7 +486,7 @@ __device__ __forceinline__ void stamp(const tc::TcParams& T, int64_t it, int e) 
   if (T.ts != nullptr && blockIdx.x < 4 && it < 64) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    T.ts[((int64_t)blockIdx.x * 64 + it) * 8 + e] = t;
+    T.ts[((int64_t)blockIdx.x * 64 + it) * 32 + e] = t;
   }
 }
 
@@ -552,6 +552,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int q = 0; q < n_kb; ++q, ++pb) {
             const int bs = (int)(pb % NBP);
             wait_empty(U(C.b_empty[bs]), pb / NBP);
+            stamp(T, it, 24 + q);
             if (T.dbg & 8) {
               arrive(U(C.b_full[bs]));
               continue;
@@ -586,11 +587,14 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int kb = 0; kb < n_kb; ++kb, ++g) {
               const uint32_t pi = pb + kb;
               const int bs = (int)(pi % NBP);
-              if (c == 0) wait_full(U(C.b_full[bs]), pi / NBP);
+              if (c == 0) {
+                wait_full(U(C.b_full[bs]), pi / NBP);
+                stamp(T, it, 12 + kb);
+              }
               const int st = (int)(g % NST);
               wait_full(U(C.a_full[st]), g / NST);
               tc::tc_fence_after();
-              if (c == 0 && kb == 0) stamp(T, it, 7);
+              if (c == 0) stamp(T, it, 8 + kb);
               const uint32_t a_hi = uA + st * tc::A_STAGE, a_lo = a_hi + tc::A_HALF;
               const uint32_t b_hi = uB + bs * tc::B_PIECE;  // hi rows 0-63, lo rows 64-127
               if (!(T.dbg & 4)) {
@@ -664,6 +668,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int kb = 0; kb < n_kb; ++kb, ++g) {
           const int st = (int)(g % NST);
           wait_empty(U(C.a_empty[st]), g / NST);
+          if (c == 0 && tid == 128) stamp(T, it, 16 + kb);
           if (!(T.dbg & 1)) {
             const uint32_t stage = uA + st * tc::A_STAGE;
 #pragma unroll
@@ -729,6 +734,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         wait_full(U(C.acc_full[ab]), cg >> 1);
         tc::tc_fence_after();
+        if (c == 0 && tid == 256) stamp(T, it, 20);
         const float s_c = tc::exp2_neg(e_c);
         float vm[32], vc[32];
 #pragma unroll
@@ -758,6 +764,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
         tc::tc_fence_before();
+        if (c == 0 && tid == 256) stamp(T, it, 21);
         arrive(U(C.acc_empty[ab]));
       }
       if (tid == 256) stamp(T, it, 4);
@@ -1028,8 +1035,8 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
   static unsigned long long* ts_buf = nullptr;
   T.ts = nullptr;
   if (dbg & 16) {
-    if (ts_buf == nullptr) cudaMalloc(&ts_buf, 4 * 64 * 8 * sizeof(unsigned long long));
-    cudaMemsetAsync(ts_buf, 0, 4 * 64 * 8 * sizeof(unsigned long long), as_stream(stream));
+    if (ts_buf == nullptr) cudaMalloc(&ts_buf, 4 * 64 * 32 * sizeof(unsigned long long));
+    cudaMemsetAsync(ts_buf, 0, 4 * 64 * 32 * sizeof(unsigned long long), as_stream(stream));
     T.ts = ts_buf;
   }
   if (n_sms == 0) {
@@ -1049,22 +1056,20 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
   const int64_t grid = T.P.ntile < n_sms ? T.P.ntile : n_sms;
   launch_pdl(tcp::partial_contract_tcp_kernel, dim3((unsigned)grid), dim3(tcp::THREADS), smem,
              as_stream(stream), T);
-  if (T.ts != nullptr) {  // debug timeline dump (CTA 0..3, first 64 tiles each), ns
-    unsigned long long h[4 * 64 * 8];
+  if (T.ts != nullptr) {  // debug timeline dump (CTA 0..3, first 64 tiles, 32 events), ns
+    static unsigned long long h[4 * 64 * 32];
     cudaStreamSynchronize(as_stream(stream));
     cudaMemcpy(h, T.ts, sizeof(h), cudaMemcpyDeviceToHost);
     static int call = 0;
     ++call;
-    const unsigned long long t0 = h[0];
-    for (int b = 0; b < 2; ++b)
-      for (int it = 0; it < 64; ++it) {
-        const unsigned long long* e = h + (b * 64 + it) * 8;
-        if (e[1] == 0) break;
-        fprintf(stderr, "TS call %d cta %d it %2d plan %7.2f mma0 %7.2f mma1 %7.2f A %7.2f epi %7.2f B %7.2f accE %7.2f a0 %7.2f\n",
-                call, b, it, (e[0] - t0) * 1e-3, (e[1] - t0) * 1e-3, (e[2] - t0) * 1e-3,
-                (e[3] - t0) * 1e-3, (e[4] - t0) * 1e-3, (e[5] - t0) * 1e-3, (e[6] - t0) * 1e-3,
-                (e[7] - t0) * 1e-3);
+    const char* path = getenv("CVB_TC_TS_FILE");
+    if (path != nullptr) {
+      FILE* f = fopen(path, call == 1 ? "wb" : "ab");
+      if (f) {
+        fwrite(h, sizeof(h), 1, f);
+        fclose(f);
       }
+    }
   }
   return check_launch("partial_contract_tcp");
 }
