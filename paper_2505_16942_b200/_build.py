@@ -60,6 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objdir = PKG / "build"
     objdir.mkdir(exist_ok=True)
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    compile_flags += os.environ.get("CVB_NVCC_EXTRA", "").split()  # variant builds only
 
     def compile_one(src: str):
         obj = objdir / (Path(src).stem + ".o")

@@ -92,6 +92,16 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b,
       "l"(a), "l"(b), "r"(ID), "r"(acc));
 }
 
+// one lane of a converged warp (elect.sync): the MMA issuer runs as a whole
+// warp so tcgen05.mma / commit issue without a per-instruction divergence loop
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(e));
+  return e != 0;
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    mbar)
@@ -568,54 +578,60 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      uint32_t pb = 0, g = 0, cg = 0;
-      for (int64_t it = 0;; ++it) {
-        const int s = (int)(it % NPL);
-        wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
-        if (C.slot[s].tile < 0) break;
-        stamp(T, it, 1);
-        const int n = C.slot[s].n_cells;
-        if (n > 0) {
-          const int n_chunks = (n + tc::M - 1) / tc::M;
-          for (int c = 0; c < n_chunks; ++c, ++cg) {
-            const int ab = cg & 1;
-            wait_empty(U(C.acc_empty[ab]), cg >> 1);
+    // the whole warp walks the rings (converged); one elected lane issues.
+    // Descriptors are built once per stage: a K=16 step advances the
+    // swizzled A start by 32 B (+2 in the descriptor's address field) and
+    // the B start by 256 B (+16).
+    uint32_t pb = 0, g = 0, cg = 0;
+    for (int64_t it = 0;; ++it) {
+      const int s = (int)(it % NPL);
+      wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
+      if (C.slot[s].tile < 0) break;
+      if (lane == 0) stamp(T, it, 1);
+      const int n = C.slot[s].n_cells;
+      if (n > 0) {
+        const int n_chunks = (n + tc::M - 1) / tc::M;
+        for (int c = 0; c < n_chunks; ++c, ++cg) {
+          const int ab = cg & 1;
+          wait_empty(U(C.acc_empty[ab]), cg >> 1);
+          tc::tc_fence_after();
+          if (c == 0 && lane == 0) stamp(T, it, 6);
+          const uint32_t d_main = tmem + ab * 128, d_corr = d_main + 64;
+          for (int kb = 0; kb < n_kb; ++kb, ++g) {
+            const uint32_t pi = pb + kb;
+            const int bs = (int)(pi % NBP);
+            if (c == 0) {
+              wait_full(U(C.b_full[bs]), pi / NBP);
+              if (lane == 0) stamp(T, it, 12 + kb);
+            }
+            const int st = (int)(g % NST);
+            wait_full(U(C.a_full[st]), g / NST);
             tc::tc_fence_after();
-            if (c == 0) stamp(T, it, 6);
-            const uint32_t d_main = tmem + ab * 128, d_corr = d_main + 64;
-            for (int kb = 0; kb < n_kb; ++kb, ++g) {
-              const uint32_t pi = pb + kb;
-              const int bs = (int)(pi % NBP);
-              if (c == 0) {
-                wait_full(U(C.b_full[bs]), pi / NBP);
-                stamp(T, it, 12 + kb);
-              }
-              const int st = (int)(g % NST);
-              wait_full(U(C.a_full[st]), g / NST);
-              tc::tc_fence_after();
-              if (c == 0) stamp(T, it, 8 + kb);
-              const uint32_t a_hi = uA + st * tc::A_STAGE, a_lo = a_hi + tc::A_HALF;
-              const uint32_t b_hi = uB + bs * tc::B_PIECE;  // hi rows 0-63, lo rows 64-127
+            if (c == 0 && lane == 0) stamp(T, it, 8 + kb);
+            const uint32_t a_hi = uA + st * tc::A_STAGE, a_lo = a_hi + tc::A_HALF;
+            const uint32_t b_hi = uB + bs * tc::B_PIECE;  // hi rows 0-63, lo rows 64-127
+            const uint64_t dah = tc::make_desc_sw128(a_hi), dal = tc::make_desc_sw128(a_lo);
+            const uint64_t dbh = tc::make_desc(b_hi, 128, (tc::KP / 8) * 128);
+            if (tc::elect_one()) {
               if (!(T.dbg & 4)) {
 #pragma unroll
                 for (int k = 0; k < tc::KP / 16; ++k) {
-                  const uint64_t dah = tc::make_desc_sw128(a_hi + k * 32);
-                  const uint64_t dal = tc::make_desc_sw128(a_lo + k * 32);
-                  const uint64_t dbh = tc::make_desc(b_hi + k * 256, 128, (tc::KP / 8) * 128);
-                    const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+                  const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
                   // cols 0-63 += A_hi B_hi (main), cols 64-127 += A_hi B_lo (corr)
-                  tc::mma_f16<tc::IDESC_N128>(d_main, dah, dbh, acc);
-                  tc::mma_f16(d_corr, dal, dbh, 1u);  // corr += A_lo B_hi
+                  tc::mma_f16<tc::IDESC_N128>(d_main, dah + 2 * k, dbh + 16 * k, acc);
+                  tc::mma_f16(d_corr, dal + 2 * k, dbh + 16 * k, 1u);  // corr += A_lo B_hi
                 }
               }
               tc::mma_commit(U(C.a_empty[st]));
               if (c == n_chunks - 1) tc::mma_commit(U(C.b_empty[bs]));
+              if (kb == n_kb - 1) tc::mma_commit(U(C.acc_full[ab]));
             }
-            tc::mma_commit(U(C.acc_full[ab]));
+            __syncwarp();
           }
-          pb += n_kb;
         }
+        pb += n_kb;
+      }
+      if (lane == 0) {
         stamp(T, it, 2);
         arrive(U(C.plan_empty[s]));
       }
