@@ -321,6 +321,11 @@ def main():
 
     main_step = step
     graph_launches = 0
+    # peak HBM covers the whole step's allocations, including the buffers a
+    # CUDA graph keeps in its private pool from capture time on
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats(dev)
+    base_alloc = torch.cuda.memory_allocated(dev)
     if args.graph:
         # the whole step (prepare + every lookup) captured once into a CUDA graph
         # over the static input/output buffers and replayed (no per-launch host
@@ -346,8 +351,6 @@ def main():
     for _ in range(args.warmup):
         main_step()
     torch.cuda.synchronize()
-    torch.cuda.reset_peak_memory_stats(dev)
-    base_alloc = torch.cuda.memory_allocated(dev)
     launches0 = _lib.launch_count()
     ms_step = timed(main_step, args.steps, 0)
     launches = _lib.launch_count() - launches0 + graph_launches * args.steps
