@@ -105,6 +105,24 @@ class _RefScenario:
         self.h, self.w, self.iters = h, w, n_iter
 
 
+def init_dist(torch, dist):
+    """One process per GPU (torchrun env).  NCCL by default; CVB_BENCH_BACKEND=gloo
+    exercises the multi-rank path with several ranks sharing one GPU (the
+    scalar reductions then run on the host)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    backend = os.environ.get("CVB_BENCH_BACKEND", "nccl")
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    return world, rank, dev, (dev if backend == "nccl" else torch.device("cpu"))
+
+
 def reference_sample(cfg: str, workers: int, rows_per_worker: int):
     """Time the reference on `workers` parallel row bands; extrapolate to the frame.
 
@@ -263,13 +281,7 @@ def main():
     from paper_2505_16942_b200.parallel import row_bands
     from paper_2505_16942_b200.sparse import sample_iteration_timed
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    world, rank, dev, red_dev = init_dist(torch, dist)
 
     def barrier():
         if world > 1:
@@ -278,7 +290,7 @@ def main():
     def allmax(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -346,7 +358,7 @@ def main():
     # ---- main measurement: inputs resident in HBM -------------------------
     # nvidia-smi samples clocks from before the warm-up to the end of the timed
     # region (the GPU is under load the whole time); it needs ~1 s to start.
-    clocks = Clocks(local).start()
+    clocks = Clocks(dev.index).start()
     time.sleep(1.5)
     for _ in range(args.warmup):
         main_step()
@@ -382,6 +394,8 @@ def main():
     # dram bytes per launch from the committed `ncu --set full` capture (or null)
     traffic_path = ROOT / "profiles" / f"ncu_traffic_{args.config}.json"
     traffic = json.loads(traffic_path.read_text()) if traffic_path.exists() else {}
+    if rows != h:  # the capture is of a full-frame launch; this rank runs a row band
+        traffic = {k: int(v * rows / h) for k, v in traffic.items() if isinstance(v, (int, float))}
     geom_path = ROOT / "profiles" / f"geometry_{args.config}.json"
     geom = json.loads(geom_path.read_text()) if geom_path.exists() else None
     out_bytes_iter = rows * w * levels * k1 * k1 * 4
@@ -579,13 +593,7 @@ def run_batch(args) -> None:
     import paper_2505_16942_b200 as cvb
     from paper_2505_16942_b200.parallel import batch_slices, gather_bands
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    world, rank, dev, red_dev = init_dist(torch, dist)
     h, w, d, r, levels, n_iter, norm = CONFIGS["C5"]
     spec = cvb.LookupSpec(r, levels, norm)
     a, b = batch_slices(args.batch, world)[rank]
@@ -628,7 +636,7 @@ def run_batch(args) -> None:
     ms = e0.elapsed_time(e1) / args.steps
     peak = torch.cuda.max_memory_allocated(dev)
     if world > 1:
-        t = torch.tensor([ms, float(peak)], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, float(peak)], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, peak = float(t[0]), int(t[1])
         dist.barrier()
