@@ -23,7 +23,7 @@ __device__ __forceinline__ int row_of(int cta, int c, int r, int nrows, int span
   const int base = (int)((hashu(cta * 7919 + c) % (uint32_t)nrows));
   return (base + (int)(hashu(cta * 131071 + c * 977 + r) % (uint32_t)span)) % nrows;
 }
-template <bool TMA>
+template <int MODE>
 __global__ void __launch_bounds__(384, 1) k(const __half* f2, const __grid_constant__ CUtensorMap tm, int nrows,
                                             int span, int nchunks, unsigned long long* out) {
   extern __shared__ uint8_t raw[];
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(384, 1) k(const __half* f2, const __grid_const
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[i])), "r"(TMA ? 1 : 128) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[i])), "r"(MODE == 1 || MODE == 3 ? 1 : MODE == 4 ? 129 : 128) : "memory");
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&empty[i])) : "memory");
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(384, 1) k(const __half* f2, const __grid_const
       }
       out[blockIdx.x] = clock64() - t0;
     }
-  } else if (!TMA && warp >= 4 && warp < 8) {
+  } else if (MODE == 0 && warp >= 4 && warp < 8) {
     const int aw = warp - 4, sub = lane >> 3, chunk = lane & 7;
     int g = 0;
     for (int c = 0; c < nchunks; ++c) {
@@ -72,7 +72,95 @@ __global__ void __launch_bounds__(384, 1) k(const __half* f2, const __grid_const
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(&full[st])) : "memory");
       }
     }
-  } else if (TMA && warp == 4) {
+  } else if (MODE == 2 && warp >= 4 && warp < 8) {
+    // LDG.128 into registers (8 lanes per row), then st.shared into the swizzled stage
+    const int aw = warp - 4, sub = lane >> 3, chunk = lane & 7;
+    int g = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int my_row = row_of(blockIdx.x, c, 32 * aw + lane, nrows, span);
+      for (int kb = 0; kb < 4; ++kb, ++g) {
+        const int st = g % NST;
+        uint4 vh[8], vl[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rl = 4 * i + sub;
+          const int r = __shfl_sync(0xffffffffu, my_row, rl);
+          const __half* src = f2 + (int64_t)r * 256 + kb * 64 + chunk * 8;
+          vh[i] = __ldg(reinterpret_cast<const uint4*>(src));
+          vl[i] = __ldg(reinterpret_cast<const uint4*>(src + plane));
+        }
+        while (!tryw(su32(&empty[st]), ((g / NST) & 1) ^ 1)) {}
+        uint8_t* stage = sm + st * STAGE;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int row = 32 * aw + 4 * i + sub;
+          *reinterpret_cast<uint4*>(stage + row * 128 + ((chunk ^ (row & 7)) << 4)) = vh[i];
+          *reinterpret_cast<uint4*>(stage + HALF + row * 128 + ((chunk ^ (row & 7)) << 4)) = vl[i];
+        }
+        arrive(su32(&full[st]));
+      }
+    }
+  } else if (MODE == 3 && warp >= 4 && warp < 8) {
+    // TMA gather4 issued by 8 lanes of each of 4 warps (4 rows per lane)
+    const int aw = warp - 4;
+    int g = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      int r[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) r[j] = row_of(blockIdx.x, c, 32 * aw + 4 * (lane & 7) + j, nrows, span);
+      for (int kb = 0; kb < 4; ++kb, ++g) {
+        const int st = g % NST;
+        while (!tryw(su32(&empty[st]), ((g / NST) & 1) ^ 1)) {}
+        if (aw == 0 && lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[st])), "r"(STAGE) : "memory");
+        if (lane < 8) {
+          const uint32_t dst = uA + st * STAGE + (32 * aw + 4 * lane) * 128;
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst), "l"(&tm), "r"(kb * 64), "r"(r[0]), "r"(r[1]),
+              "r"(r[2]), "r"(r[3]), "r"(su32(&full[st])) : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst + HALF), "l"(&tm), "r"(kb * 64), "r"(r[0] + nrows),
+              "r"(r[1] + nrows), "r"(r[2] + nrows), "r"(r[3] + nrows), "r"(su32(&full[st])) : "memory");
+        }
+      }
+    }
+  } else if (MODE == 4 && warp >= 4 && warp < 8) {
+    // hi half by TMA gather4 (lanes 0-7), lo half by LDGSTS (all lanes, noinc)
+    const int aw = warp - 4, sub = lane >> 3, chunk = lane & 7;
+    int g = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      int r[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) r[j] = row_of(blockIdx.x, c, 32 * aw + 4 * (lane & 7) + j, nrows, span);
+      const int my_row = row_of(blockIdx.x, c, 32 * aw + lane, nrows, span);
+      for (int kb = 0; kb < 4; ++kb, ++g) {
+        const int st = g % NST;
+        while (!tryw(su32(&empty[st]), ((g / NST) & 1) ^ 1)) {}
+        if (aw == 0 && lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[st])), "r"(HALF) : "memory");
+        const uint32_t stage = uA + st * STAGE;
+        if (lane < 8) {
+          const uint32_t dst = stage + (32 * aw + 4 * lane) * 128;
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst), "l"(&tm), "r"(kb * 64), "r"(r[0]), "r"(r[1]),
+              "r"(r[2]), "r"(r[3]), "r"(su32(&full[st])) : "memory");
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rl = 4 * i + sub;
+          const int rr = __shfl_sync(0xffffffffu, my_row, rl);
+          const int row = 32 * aw + rl;
+          const uint32_t dst = stage + HALF + row * 128 + ((chunk ^ (row & 7)) << 4);
+          const __half* src = f2 + (int64_t)rr * 256 + kb * 64 + chunk * 8 + plane;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(&full[st])) : "memory");
+      }
+    }
+  } else if (MODE == 1 && warp == 4) {
     int g = 0;
     for (int c = 0; c < nchunks; ++c) {
       int r[4];
@@ -154,8 +242,9 @@ int main() {
   unsigned long long hh[148];
   const int smem = NST * STAGE + 1024, nch = 400;
   for (int span : {1 << 30, 4096, 512}) {
-    for (int tma = 0; tma < 2; ++tma) {
-      auto kern = tma ? k<true> : k<false>;
+    for (int tma = 0; tma < 5; ++tma) {
+      if (tma == 2 || tma == 1) continue;
+      auto kern = tma == 0 ? k<0> : tma == 1 ? k<1> : tma == 2 ? k<2> : tma == 3 ? k<3> : k<4>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
       kern<<<148, 384, smem>>>(f2, tm, nrows, span > nrows ? nrows : span, nch, d);
@@ -164,7 +253,7 @@ int main() {
       cudaEventRecord(e1); cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
       const double bytes = 148.0 * nch * 4 * STAGE;
-      printf("%s span %8d rows: %.3f ms, %.0f GB/s into smem (%s)\n", tma ? "TMA gather4" : "LDGSTS     ",
+      printf("%s span %8d rows: %.3f ms, %.0f GB/s into smem (%s)\n", tma == 1 ? "TMA gather4" : tma == 2 ? "LDG+STS    " : tma == 3 ? "gather4 x32" : tma == 4 ? "hi TMA+lo LDGSTS" : "LDGSTS     ",
              span > nrows ? nrows : span, ms, bytes / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
     }
   }

@@ -18,7 +18,7 @@ for ln in lines:
     if "B producer: F1 pieces" in ln: role = "B"
     elif "MMA issuer ---" in ln: role = "MMA"
     elif "plan loader: one bulk" in ln: role = "L"
-    elif "A producers: cp.async" in ln: role = "A"
+    elif "A producers:" in ln: role = "A"
     elif "epilogue (128 threads" in ln: role = "E"
     m = re.match(r"^(\s*)(wait_(full|empty)\(U\(C\.(\w+)\[.*)$", ln)
     if m and role:
