@@ -7,6 +7,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <atomic>
 #include <utility>
 
 #include "../../include/corrvol_b200.h"
@@ -57,6 +58,19 @@ static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 b
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Function attributes live in the current device's context: opt each kernel
+// into its dynamic shared memory once per device (call sites keep `done`).
+template <typename Kernel>
+static inline void ensure_max_smem(std::atomic<uint64_t>& done, Kernel kernel, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(done.load(std::memory_order_acquire) & bit)) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done.fetch_or(bit, std::memory_order_release);
+  }
+}
 
 // ---- arithmetic ------------------------------------------------------------
 // Reference dot arithmetic: fp32, ascending channel, every multiply and add

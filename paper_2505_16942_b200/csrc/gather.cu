@@ -391,13 +391,9 @@ __global__ void __launch_bounds__(WARPS * 32)
 
 template <bool STRICT, int RADIUS>
 static void launch_one(const PartialParams& P, float* out, int l0, int nl, cudaStream_t s) {
-  static bool attr = false;
+  static std::atomic<uint64_t> attr{0};
   const int smem = (int)sizeof(gather::Shared);
-  if (!attr) {
-    cudaFuncSetAttribute(gather::gather_kernel<STRICT, RADIUS>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  ensure_max_smem(attr, gather::gather_kernel<STRICT, RADIUS>, smem);
   gather::gather_kernel<STRICT, RADIUS>
       <<<(unsigned)(2 * P.ntile), gather::WARPS * 32, smem, s>>>(P, out, l0, nl);
 }

@@ -229,13 +229,9 @@ __global__ void __launch_bounds__(WARPS * 32, 2) gather_fast_kernel(PartialParam
 }  // namespace gfast
 
 int launch_gather_fast_r4(const PartialParams& P, float* out, cudaStream_t s) {
-  static bool attr = false;
+  static std::atomic<uint64_t> attr{0};
   const int smem = (int)sizeof(gfast::Shared);
-  if (!attr) {
-    cudaFuncSetAttribute(gfast::gather_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         smem);
-    attr = true;
-  }
+  ensure_max_smem(attr, gfast::gather_fast_kernel, smem);
   for (int l0 = 0; l0 < P.levels; l0 += gfast::MAXL) {
     const int nl = min(gfast::MAXL, P.levels - l0);
     launch_pdl(gfast::gather_fast_kernel, dim3((unsigned)P.ntile), dim3(gfast::WARPS * 32), smem,

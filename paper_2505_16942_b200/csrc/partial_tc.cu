@@ -1040,8 +1040,7 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
     if (used) CVB_REQUIRE(T.f2s[l], "partial_contract_tc: null level pointer");
   }
   if (T.P.ntile == 0) return CVB_OK;
-  static int n_sms = 0;
-  static bool attr = false;
+  static int n_sms = 0;  // 148 on every B200
   static int dbg = -1;
   if (dbg < 0) {
     const char* e = getenv("CVB_TC_DEBUG");
@@ -1061,11 +1060,8 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
     cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const size_t smem = tcp::smem_bytes();
-  if (!attr) {
-    cudaFuncSetAttribute(tcp::partial_contract_tcp_kernel,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  ensure_max_smem(attr, tcp::partial_contract_tcp_kernel, (int)smem);
   launch_pdl(tcp::plan_kernel, dim3((unsigned)ceil_div(T.P.ntile, tcp::PLAN_WARPS)),
              dim3(tcp::PLAN_WARPS * 32), 0, as_stream(stream), T.P);
   if ((st = check_launch("partial_plan")) != CVB_OK) return st;
