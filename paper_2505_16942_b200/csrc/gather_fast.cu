@@ -159,14 +159,21 @@ __global__ void __launch_bounds__(WARPS * 32, 2) gather_fast_kernel(PartialParam
       if (++xs == cw) xs = 0;
     }
     float* o = O + (q * nlev + li) * KK;
+    // patch rows 0-3, then 4-6 and 7-9: a pass's last row is the next pass's
+    // first, carried in registers (each cache row is loaded once)
+    float v[4][S];
+    int sy = (ay - R) % ch;
+    if (sy < 0) sy += ch;
 #pragma unroll 1
     for (int pass = 0; pass < 3; ++pass) {
       const int y0 = ay - R + 3 * pass;
-      int sy = y0 % ch;
-      if (sy < 0) sy += ch;
-      float v[4][S];
+      if (pass > 0) {
+#pragma unroll
+        for (int i = 0; i < S; ++i) v[0][i] = v[3][i];
+      }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
+        if (pass > 0 && j == 0) continue;
         const int gy = y0 + j;
         const bool rin = status == ST_OK && gy >= 0 && gy < th;
         const float* prow = plane + (int64_t)(sy * cw) * QG;
