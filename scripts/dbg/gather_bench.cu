@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(384, 1) k(const __half* f2, const __grid_const
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[i])), "r"(MODE == 1 || MODE == 3 ? 1 : MODE == 4 ? 129 : 128) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[i])), "r"(MODE == 1 || MODE == 3 ? 1 : MODE == 4 ? 129 : MODE == 5 ? 256 : 128) : "memory");
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&empty[i])) : "memory");
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -124,6 +124,29 @@ __global__ void __launch_bounds__(384, 1) k(const __half* f2, const __grid_const
               " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst + HALF), "l"(&tm), "r"(kb * 64), "r"(r[0] + nrows),
               "r"(r[1] + nrows), "r"(r[2] + nrows), "r"(r[3] + nrows), "r"(su32(&full[st])) : "memory");
         }
+      }
+    }
+  } else if (MODE == 5 && (warp >= 4)) {
+    // LDGSTS from 8 warps (warps 4-11), 16 rows each
+    const int aw = warp - 4, sub = lane >> 3, chunk = lane & 7;
+    int g = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int my_row = row_of(blockIdx.x, c, 16 * aw + (lane & 15), nrows, span);
+      for (int kb = 0; kb < 4; ++kb, ++g) {
+        const int st = g % NST;
+        while (!tryw(su32(&empty[st]), ((g / NST) & 1) ^ 1)) {}
+        const uint32_t stage = uA + st * STAGE;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rl = 4 * i + sub;
+          const int r = __shfl_sync(0xffffffffu, my_row, rl);
+          const int row = 16 * aw + rl;
+          const uint32_t dst = stage + row * 128 + ((chunk ^ (row & 7)) << 4);
+          const __half* src = f2 + (int64_t)r * 256 + kb * 64 + chunk * 8;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + HALF), "l"(src + plane) : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(&full[st])) : "memory");
       }
     }
   } else if (MODE == 4 && warp >= 4 && warp < 8) {
@@ -242,9 +265,9 @@ int main() {
   unsigned long long hh[148];
   const int smem = NST * STAGE + 1024, nch = 400;
   for (int span : {1 << 30, 4096, 512}) {
-    for (int tma = 0; tma < 5; ++tma) {
-      if (tma == 2 || tma == 1) continue;
-      auto kern = tma == 0 ? k<0> : tma == 1 ? k<1> : tma == 2 ? k<2> : tma == 3 ? k<3> : k<4>;
+    for (int tma = 0; tma < 6; ++tma) {
+      if (tma == 2 || tma == 1 || tma == 4) continue;
+      auto kern = tma == 0 ? k<0> : tma == 1 ? k<1> : tma == 2 ? k<2> : tma == 3 ? k<3> : tma == 4 ? k<4> : k<5>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
       kern<<<148, 384, smem>>>(f2, tm, nrows, span > nrows ? nrows : span, nch, d);
@@ -253,7 +276,7 @@ int main() {
       cudaEventRecord(e1); cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
       const double bytes = 148.0 * nch * 4 * STAGE;
-      printf("%s span %8d rows: %.3f ms, %.0f GB/s into smem (%s)\n", tma == 1 ? "TMA gather4" : tma == 2 ? "LDG+STS    " : tma == 3 ? "gather4 x32" : tma == 4 ? "hi TMA+lo LDGSTS" : "LDGSTS     ",
+      printf("%s span %8d rows: %.3f ms, %.0f GB/s into smem (%s)\n", tma == 1 ? "TMA gather4" : tma == 2 ? "LDG+STS    " : tma == 3 ? "gather4 x32" : tma == 4 ? "hi TMA+lo LDGSTS" : tma == 5 ? "LDGSTS 8 warps" : "LDGSTS     ",
              span > nrows ? nrows : span, ms, bytes / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
     }
   }
