@@ -20,9 +20,9 @@
 //     bulk async copy (cp.async.bulk + mbarrier complete_tx) into a ring of
 //     pieces, so the next tile's first pieces land while the current tile's
 //     last chunk still runs; A rows (gathered new bbox cells of all levels,
-//     128 per chunk) stream through an 8-stage cp.async ring in the canonical
-//     K-major no-swizzle core-matrix layout (8 rows x 16 B) that never drains
-//     between tiles;
+//     128 per chunk) stream by cp.async (8 lanes per 128-byte row) through a
+//     4-stage ring of 128B-swizzled K=64 stages (32 KB: hi + lo) that never
+//     drains between tiles;
 //   * the epilogue reads TMEM with tcgen05.ld, combines main + 2^-11 corr,
 //     removes the power-of-two scales and writes each cell's 64 query costs
 //     into its cache slot.
