@@ -441,3 +441,20 @@ def test_graph_mode_equals_eager(cuda):
         got = graphed(cvb.CentroidField(ct)).values
         assert torch.equal(got, want)
     assert graphed._graph is not None and graphed.state.iteration == 5
+
+
+@pytest.mark.parametrize("d,tc", [(256, True), (264, False), (320, False)])
+def test_feature_width_selects_contraction_and_holds_gates(cuda, d, tc):
+    """D <= 256 contracts on tcgen05 (split fp16); wider features take the FP32
+    FFMA contraction of the same tiler — both within the reference gates."""
+    spec = cvb.LookupSpec(4, 3)
+    sc = cvb.gen_scenario(5, (24, 40, d), 3, spec)
+    f1 = cvb.FeatureMap(torch.from_numpy(sc.f1).to(cuda))
+    f2 = cvb.FeatureMap(torch.from_numpy(sc.f2).to(cuda))
+    st = cvb.init_state(f1, f2, spec)
+    assert st.tc == tc
+    for coords in sc.centroid_fields:
+        want = O.lookup(sc.f1, sc.f2, coords, spec.radius, spec.levels)
+        got = cvb.sample_iteration(st, cvb.CentroidField(torch.from_numpy(coords).to(cuda))).numpy()
+        dev_, ns = _gates(got, want, sc.f1, sc.f2)
+        assert dev_ <= REF_GATE and ns <= NS_GATE, (d, dev_, ns)
