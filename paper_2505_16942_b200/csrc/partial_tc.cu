@@ -430,11 +430,13 @@ __device__ __forceinline__ CellRef cell_of(int g, const TilePlan* plans, const i
 //   warp 0       B producer: one 16 KB bulk copy per F1 K-piece into an
 //                NBP-deep piece ring (a piece is released after the last
 //                chunk of its tile has consumed it)
-//   warp 1       MMA issuer (one thread): 3 tcgen05.mma per K=16 step
+//   warp 1       MMA issuer (converged warp, one elected lane issues): two
+//                tcgen05.mma per K=16 step
 //   warp 2       plan loader: the tile's PlanRec (window-union tiler output
 //                of every level, computed for all tiles at once by
 //                plan_kernel) via one bulk copy into an NPL-deep slot ring
-//   warps 4-7    A producers: per chunk and 64-channel K block, every new
+//   warps 4-7,   A producers (16 rows each): per chunk and 64-channel K
+//   12-15        block, every new
 //                cell's hi and lo 128-byte rows via cp.async (full L2 lines)
 //                into a 128B-swizzled NST-stage ring, completion tracked by
 //                cp.async.mbarrier.arrive.noinc
@@ -446,7 +448,9 @@ namespace tcp {
 constexpr int NST = 4;              // A stages (32 KB each: hi + lo, 128 rows x 64 channels)
 constexpr int NBP = 5;              // F1 pieces in the ring (16 KB each)
 constexpr int NPL = 4;              // plan slots
-constexpr int THREADS = 384;
+constexpr int THREADS = 512;
+constexpr int A_WARPS = 8;             // A producers: warps 4-7 and 12-15
+constexpr int A_ROWS = 128 / A_WARPS;  // A rows per producer warp
 constexpr uint32_t SPIN_LIMIT = 1u << 24;  // watchdog: trap instead of hanging
 
 struct Ctl {
@@ -525,14 +529,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (tid == 32) {
     for (int i = 0; i < NPL; ++i) {
       tc::mbar_init(U(C.plan_full[i]), 1);
-      tc::mbar_init(U(C.plan_empty[i]), 1 + 1 + 128 + 128);
+      tc::mbar_init(U(C.plan_empty[i]), 1 + 1 + 32 * A_WARPS + 128);
     }
     for (int i = 0; i < NBP; ++i) {
       tc::mbar_init(U(C.b_full[i]), 1);
       tc::mbar_init(U(C.b_empty[i]), 1);
     }
     for (int i = 0; i < NST; ++i) {
-      tc::mbar_init(U(C.a_full[i]), 128);
+      tc::mbar_init(U(C.a_full[i]), 32 * A_WARPS);
       tc::mbar_init(U(C.a_empty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -654,14 +658,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         stamp(T, it, 0);
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if ((warp >= 4 && warp < 8) || warp >= 12) {
     // ---------------- A producers: cp.async of the new cells ----------------
-    // warp aw owns A rows 32aw..32aw+31; per 4-row group one warp instruction
+    // warp aw owns A rows A_ROWS*aw ..+A_ROWS-1 (eight warps: per-chunk cell
+    // decoding and issue run in parallel; -3% at iteration 0 against four);
+    // per 4-row group one warp instruction
     // moves 4 full 128-byte rows (8 lanes x 16 B each, full L2 lines) into
     // the 128B-swizzled stage; completion is signalled per thread with
     // cp.async.mbarrier.arrive.noinc, so no producer thread ever waits on
     // its own copies.
-    const int aw = warp - 4;
+    const int aw = warp < 8 ? warp - 4 : warp - 8;
     const int sub = lane >> 3, chunk = lane & 7;
     uint32_t g = 0;  // A stages issued
     for (int64_t it = 0;; ++it) {
@@ -673,7 +679,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int n_chunks = (n + tc::M - 1) / tc::M;
       for (int c = 0; c < n_chunks; ++c) {
         // source row of A row 32aw + lane (hi plane; lo = hi + plane)
-        const int gi = c * tc::M + 32 * aw + lane;
+        const int gi = c * tc::M + A_ROWS * aw + (lane % A_ROWS);
         const __half* my_hi = nullptr;
         int64_t my_plane = 0;
         if (gi < n) {
@@ -688,13 +694,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (!(T.dbg & 1)) {
             const uint32_t stage = uA + st * tc::A_STAGE;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int rl = 4 * i + sub;  // row within the warp's 32
+            for (int i = 0; i < A_ROWS / 4; ++i) {
+              const int rl = 4 * i + sub;  // row within the warp's A_ROWS
               const __half* hi = reinterpret_cast<const __half*>(
                   __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_hi), rl));
               const int64_t pl = __shfl_sync(0xffffffffu, my_plane, rl);
               if (hi != nullptr) {
-                const int row = 32 * aw + rl;
+                const int row = A_ROWS * aw + rl;
                 const uint32_t dst = stage + row * 128 + ((chunk ^ (row & 7)) << 4);
                 const __half* src = hi + kb * tc::KP + chunk * 8;
                 tc::cp_async16(dst, src);
@@ -712,7 +718,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (tid == 128) stamp(T, it, 3);
       arrive(U(C.plan_empty[s]));
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 8 && warp < 12) {
     // ---------------- epilogue (128 threads = TMEM lanes) ----------------
     const int ep = tid - 256;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
