@@ -27,7 +27,11 @@ for r in raw[2:]:
     print("==", r[h.index("Kernel Name")][:60])
     for key in ("dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
                 "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
-                "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active"):
+                "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
+                # tcgen05: tensor-pipe busy time, its shared-memory operand reads, TMEM traffic
+                "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+                "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+                "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"):
         if key in h:
             print(f"   {key} = {r[h.index(key)]} {raw[1][h.index(key)]}")
     items = []
