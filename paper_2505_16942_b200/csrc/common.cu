@@ -22,7 +22,9 @@ bool pdl_enabled() {
   static int on = -1;
   if (on < 0) {
     // measured on B200 at C4: 0.94 vs 0.77 ms/iter with PDL on (early-launched
-    // grids hold SM resources while they wait), so it is opt-in (CVB_PDL=1)
+    // grids hold SM resources while they wait); re-measured at 0.83 vs 0.655
+    // with quarter-tile sampler CTAs, also with the triggers moved to the end
+    // of each kernel's work — so it stays opt-in (CVB_PDL=1)
     const char* e = getenv("CVB_PDL");
     on = (e != nullptr && e[0] == '1') ? 1 : 0;
   }
