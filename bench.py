@@ -468,10 +468,15 @@ def main():
         compare["ondemand_ms_per_iter"] = round(timed(lambda: step("ondemand"), 1, 1) / n_iter, 3)
         compare["partial_nocache_ms_per_iter"] = round(
             timed(lambda: step("partial", cache=False), 1, 1) / n_iter, 3)
+        torch.cuda.empty_cache()
         free, _ = torch.cuda.mem_get_info(dev)
-        if dense_bytes < 0.85 * free:
+        try:
+            if dense_bytes >= 0.85 * free:
+                raise MemoryError
             compare["dense_ms_per_iter"] = round(timed(lambda: step("dense"), 1, 1) / n_iter, 3)
-        else:
+        except (MemoryError, torch.cuda.OutOfMemoryError):
+            # reported the way harness.py:330-333 reports a dense OOM
+            torch.cuda.empty_cache()
             compare["dense"] = {"oom": True, "bytes": dense_bytes, "free_bytes": free}
     torch.cuda.synchronize()
 
