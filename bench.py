@@ -123,6 +123,31 @@ def init_dist(torch, dist):
     return world, rank, dev, (dev if backend == "nccl" else torch.device("cpu"))
 
 
+def scenario_tensors(torch, dist, world, rank, red_dev, h, w, d, n_iter, spec, seed=0):
+    """(f1 [H,W,D], f2 [H,W,D], coords [N,H,W,2] f32) as host tensors on every
+    rank: generated once on rank 0 (gen_scenario recipe, fp32 centroids) and
+    broadcast from it."""
+    if rank == 0:
+        import paper_2505_16942_b200 as cvb
+
+        sc = cvb.gen_scenario(seed, (h, w, d), n_iter, spec, coords_dtype=np.float32)
+        f1 = torch.from_numpy(sc.f1)
+        f2 = torch.from_numpy(sc.f2)
+        co = torch.from_numpy(np.stack(sc.centroid_fields))
+    else:
+        f1 = torch.empty((h, w, d), dtype=torch.float32)
+        f2 = torch.empty((h, w, d), dtype=torch.float32)
+        co = torch.empty((n_iter, h, w, 2), dtype=torch.float32)
+    if world > 1:
+        out = []
+        for t in (f1, f2, co):
+            buf = t.to(red_dev)
+            dist.broadcast(buf, src=0)
+            out.append(buf.cpu() if buf.is_cuda else buf)
+        f1, f2, co = out
+    return f1, f2, co
+
+
 def reference_sample(cfg: str, workers: int, rows_per_worker: int):
     """Time the reference on `workers` parallel row bands; extrapolate to the frame.
 
@@ -142,7 +167,8 @@ def reference_sample(cfg: str, workers: int, rows_per_worker: int):
         _REF_SC = (cv, _RefScenario(cfg))
     sc = _REF_SC[1]
     # disjoint bands spread over the frame, starting at multiples of 8 rows
-    n_slots = max(1, sc.h // rows_per_worker)
+    # (the last one may be shorter); with enough workers they cover the frame
+    n_slots = max(1, -(-sc.h // rows_per_worker))
     workers = min(workers, n_slots)
     picks = sorted({int(round(i * (n_slots - 1) / max(1, workers - 1))) for i in range(workers)})
     if workers == 1:
@@ -160,48 +186,196 @@ def reference_sample(cfg: str, workers: int, rows_per_worker: int):
     prep = statistics.mean(r[0] for r in res)
     iters = statistics.mean(r[1] for r in res)
     rows_done = sum(b - a for a, b in bands)
-    frame_s = prep + iters * sc.h / rows_done
+    # bands covering the frame run concurrently: the frame takes the slowest
+    # band; otherwise the frame needs h / rows_done rounds of the sampled bands
+    frame_s = (prep + max(r[1] for r in res) if rows_done >= sc.h
+               else prep + iters * sc.h / rows_done)
     return {"ms_per_iter": 1e3 * frame_s / sc.iters, "frame_s": frame_s, "wall_s": wall,
             "prep_s": prep, "iters_s_per_band": iters, "bands": bands, "cores": workers,
             "iterations": sc.iters}
 
 
+def workload(cfg: str, batch: int = 0) -> str:
+    """The `config.workload` string; identical in both arms."""
+    h, w, d, r, levels, n_iter, norm = CONFIGS[cfg]
+    pairs = f"batch of {batch} image pairs" if cfg == "C5" else "one image pair"
+    return (f"{cfg} {h}x{w} features D={d} L={levels} r={r} {n_iter} iterations"
+            f"{' normalize' if norm else ''}, {pairs} per step")
+
+
+def host_info() -> dict:
+    """Host cores the CPU legs can use (nproc) plus the lscpu model line."""
+    info = {"nproc": os.cpu_count(), "affinity_cores": len(os.sched_getaffinity(0))}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k.strip()] = v.strip()
+    except Exception:
+        pass
+    return info
+
+
+def _ref_variant_times(cfg: str) -> dict:
+    """The reference's three samplers on ONE core (harness.py:304-437):
+    full runs at C1; at larger configs the partial sampler on a 32-row band
+    (all iterations) and on-demand on an 8-row band (first 2 iterations), both
+    extrapolated linearly in rows (and iterations); dense is reported
+    infeasible when its volume exceeds the reference bench's dense limit
+    (DEFAULT_DENSE_LIMIT_BYTES = 2 GiB, harness.py:33,330-333)."""
+    from oracle import import_reference
+
+    cv = import_reference()
+    if cv is None:
+        raise RuntimeError("oracle/_ref not built")
+    h, w, d, r, levels, n_iter, norm = CONFIGS[cfg]
+    sc = _RefScenario(cfg)
+    spec = cv.LookupSpec(r, levels, norm)
+    cents = [c.astype(np.float64) for c in sc.centroid_fields]
+    full = cfg == "C1"
+    res = {}
+    # partial
+    a, b = (0, h) if full else (h // 2 // 8 * 8, h // 2 // 8 * 8 + 32)
+    f1 = cv.FeatureMap(values=sc.f1[a:b])
+    f2 = cv.FeatureMap(values=sc.f2)
+    t0 = time.perf_counter()
+    st = cv.init_state(f1, f2, spec, 8, backend="cython")
+    t1 = time.perf_counter()
+    for c in cents:
+        cv.sample_iteration(st, cv.CentroidField(coords=c[a:b]))
+    t2 = time.perf_counter()
+    frame_s = (t1 - t0) + (t2 - t1) * h / (b - a)
+    res["partial"] = {"ms_per_iter": 1e3 * frame_s / n_iter, "rows": [a, b],
+                      "iterations": n_iter, "measured_s": t2 - t0,
+                      "extrapolated": not full}
+    # on-demand
+    a, b = (0, h) if full else (h // 2 // 8 * 8, h // 2 // 8 * 8 + 8)
+    its = n_iter if full else 2
+    f1 = cv.FeatureMap(values=sc.f1[a:b])
+    t0 = time.perf_counter()
+    pyr = cv.build_feature_pyramid(f2, levels)
+    t1 = time.perf_counter()
+    for c in cents[:its]:
+        cv.lookup_on_demand(f1, pyr, cv.CentroidField(coords=c[a:b]), spec, backend="cython")
+    t2 = time.perf_counter()
+    frame_s = (t1 - t0) + (t2 - t1) * (h / (b - a)) * (n_iter / its)
+    res["ondemand"] = {"ms_per_iter": 1e3 * frame_s / n_iter, "rows": [a, b],
+                       "iterations": its, "measured_s": t2 - t0, "extrapolated": not full}
+    # dense (pool_features build + lookups, the bench's mode, harness.py:336-338)
+    est = cv.estimate_dense_bytes((h, w), (h, w), levels)
+    limit = 2 * 2 ** 30
+    if est > limit:
+        res["dense"] = {"oom": True, "bytes": est, "limit_bytes": limit,
+                        "note": "infeasible: reported as harness.py:330-333 reports it"}
+    else:
+        f1 = cv.FeatureMap(values=sc.f1)
+        t0 = time.perf_counter()
+        vol = cv.build_volume_pyramid(f1, f2, levels, mode="pool_features", backend="cython")
+        t1 = time.perf_counter()
+        for c in cents:
+            cv.lookup_dense(vol, cv.CentroidField(coords=c), spec)
+        t2 = time.perf_counter()
+        res["dense"] = {"ms_per_iter": 1e3 * (t2 - t0) / n_iter, "build_s": t1 - t0,
+                        "iterations": n_iter, "measured_s": t2 - t0, "extrapolated": False}
+    return res
+
+
 def cpu_baseline_worker(cfg: str) -> None:
-    out = reference_sample(cfg, 1, 32)
-    print(json.dumps(out))
+    print(json.dumps(_ref_variant_times(cfg)))
+
+
+def _ref_cores(cfg: str) -> int:
+    """Worker processes for the reference arm: every host core, bounded by host
+    memory (each worker holds the fmap2 pyramid and its patch-major copies,
+    about 3x fmap2's bytes) and by the frame's 8-row bands."""
+    h, w, d = CONFIGS[cfg][:3]
+    cores = min(len(os.sched_getaffinity(0)), -(-h // 8))
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+        cores = max(1, min(cores, int(avail * 0.6 // (3 * h * w * d * 4))))
+    except (ValueError, OSError):
+        cores = min(cores, 16)
+    return cores
 
 
 def run_reference_arm(args) -> None:
+    """The reference's own CPU partial sampler on all usable host cores.
+
+    One step = one bounded sample of the workload: every worker runs the
+    reference (init_state + all iterations) on its own 8-row band of the
+    frame, disjoint bands spread over the frame.  `ms_per_step` is the
+    measured wall time of that sample; `value` (ms per lookup iteration of the
+    whole frame) scales the per-band iteration time by frame rows / sampled
+    rows — `extrapolation` says by how much (1.0 when the bands cover the
+    frame)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    # one process per core on disjoint 8-row bands; capped at 16 processes so
-    # the per-process fmap2 pyramid + patch-major copies fit in host memory
-    cores = min(len(os.sched_getaffinity(0)), 16)
-    h, w, d, r, levels, n_iter, norm = CONFIGS[args.config]
-    times = []
+    cfg = "C3" if args.config == "C5" else args.config
+    cores = _ref_cores(cfg)
+    h, w, d, r, levels, n_iter, norm = CONFIGS[cfg]
+    vals, walls = [], []
+    res = None
     for i in range(args.warmup + args.steps):
-        res = reference_sample(args.config, cores, 8)
+        res = reference_sample(cfg, cores, 8)
         cores = res["cores"]
         if i >= args.warmup:
-            times.append(res["ms_per_iter"])
-    v = statistics.mean(times)
+            vals.append(res["ms_per_iter"])
+            walls.append(res["wall_s"])
+    rows_done = sum(b - a for a, b in res["bands"])
+    v = statistics.mean(vals) * (args.batch if args.config == "C5" else 1)
     sample = (f"reference corrvol 0.1.0 partial sampler (B=8, cython lane), {cores} processes x "
-              f"8-row bands of {args.config} ({h}x{w}, D={d}, L={levels}, r={r}), "
-              f"{n_iter} iterations each, extrapolated linearly in rows to the full frame")
+              f"one 8-row band each ({rows_done} of {h} rows of {cfg}), all {n_iter} iterations "
+              f"per band; value = per-band iteration time x {h}/{rows_done} rows"
+              + (f" x {args.batch} pairs" if args.config == "C5" else ""))
     line = {
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms/iter",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(v * n_iter, 3), "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config} {h}x{w} D={d} L={levels} r={r} "
-                               f"{n_iter} iterations", "parallelism": f"{cores} CPU processes"},
+        "ms_per_step": round(1e3 * statistics.mean(walls), 3), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload(args.config, args.batch),
+                   "parallelism": f"{cores} CPU processes"},
+        "extrapolation": {"sampled_rows": rows_done, "frame_rows": h,
+                          "factor": round(h / rows_done, 4)},
+        "host": host_info(),
         "cpu_baseline": {"value": round(v, 3), "unit": "ms/iter", "cores": cores,
                          "kind": "reference", "sample": sample},
         "e2e": {"value": round(v, 3), "unit": "ms/iter", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg: str) -> dict:
+    """`cpu_baseline` of the B200 arm: the reference's dense, on-demand and
+    partial samplers timed on ONE host core (taskset -c 0) in a subprocess;
+    `value` is the partial sampler (the path this build replaces)."""
+    try:
+        res = subprocess.run(["taskset", "-c", "0", sys.executable, str(ROOT / "bench.py"),
+                              "--cpu-baseline-worker", cfg],
+                             capture_output=True, text=True, timeout=900)
+        ref = json.loads(res.stdout.strip().splitlines()[-1])
+        p = ref["partial"]
+        parts = []
+        for name in ("partial", "ondemand", "dense"):
+            v = ref[name]
+            if v.get("oom"):
+                parts.append(f"dense infeasible ({v['bytes'] / 1e9:.1f} GB volume)")
+            else:
+                how = (f"rows {v['rows'][0]}..{v['rows'][1]}, {v['iterations']} iterations, "
+                       "extrapolated" if v.get("extrapolated") else "full frame, all iterations")
+                parts.append(f"{name} {v['ms_per_iter']:.1f} ms/iter ({how})")
+        return {"value": round(p["ms_per_iter"], 3), "unit": "ms/iter", "cores": 1,
+                "kind": "reference",
+                "sample": f"reference corrvol 0.1.0 (cython lane), 1 core (taskset -c 0), "
+                          f"{cfg}: " + "; ".join(parts),
+                "variants": {k: {kk: (round(vv, 3) if isinstance(vv, float) else vv)
+                                 for kk, vv in v.items()} for k, v in ref.items()},
+                "host": host_info()}
+    except Exception as exc:  # report, never fake
+        return {"value": None, "unit": "ms/iter", "cores": 1, "kind": "reference",
+                "sample": f"failed: {type(exc).__name__}: {exc}"[:300]}
 
 
 # ---------------------------------------------------------------------------
@@ -296,12 +470,17 @@ def main():
 
     h, w, d, r, levels, n_iter, norm = CONFIGS[args.config]
     spec = cvb.LookupSpec(r, levels, norm)
-    sc = cvb.gen_scenario(0, (h, w, d), n_iter, spec, coords_dtype=np.float32)
+    # rank 0 generates the pair; fmap2 (replicated) and the fmap1 / centroid
+    # rows are broadcast to the other ranks (NCCL over NVLink, or gloo on the
+    # host), each rank keeping its query-row band
+    f1_all, f2_all, co_all = scenario_tensors(torch, dist, world, rank, red_dev, h, w, d, n_iter,
+                                              spec)
     a, b = row_bands(h, world)[rank]
     rows = b - a
-    f1_host = torch.from_numpy(np.ascontiguousarray(sc.f1[a:b]))
-    f2_host = torch.from_numpy(sc.f2)
-    co_host = [torch.from_numpy(np.ascontiguousarray(c[a:b])) for c in sc.centroid_fields]
+    f1_host = f1_all[a:b].contiguous()
+    f2_host = f2_all
+    co_host = [co_all[i, a:b].contiguous() for i in range(n_iter)]
+    del f1_all, co_all
     f1_dev = f1_host.to(dev)
     f2_dev = f2_host.to(dev)
     co_dev = [c.to(dev) for c in co_host]
@@ -523,7 +702,7 @@ def main():
                 b_.record_stream(d2h_stream)
             main.wait_stream(d2h_stream)
 
-        e2e_steps = max(1, min(args.steps, 3))
+        e2e_steps = args.steps
         ms_e2e = timed(e2e_step, e2e_steps, 1)
         e2e = {"value": round(ms_e2e / n_iter, 3), "unit": "ms/iter",
                "h2d_bytes_per_step": (f1_host.numel() + f2_host.numel()) * 4 +
@@ -537,21 +716,7 @@ def main():
     # ---- CPU baseline (rank 0, N=1) ----------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            res = subprocess.run(["taskset", "-c", "0", sys.executable, str(ROOT / "bench.py"),
-                                  "--cpu-baseline-worker", args.config],
-                                 capture_output=True, text=True, timeout=600)
-            ref = json.loads(res.stdout.strip().splitlines()[-1])
-            cpu = {"value": round(ref["ms_per_iter"], 3), "unit": "ms/iter", "cores": 1,
-                   "kind": "reference",
-                   "sample": f"reference corrvol 0.1.0 partial sampler (B=8, cython lane) on "
-                             f"rows {ref['bands'][0][0]}..{ref['bands'][0][1]} of {args.config}, "
-                             f"{ref['iterations']} iterations, 1 core (taskset -c 0); prep "
-                             f"{ref['prep_s']:.1f}s + band iterations {ref['iters_s_per_band']:.1f}s "
-                             f"extrapolated linearly in rows to the full frame"}
-        except Exception as exc:  # report, never fake
-            cpu = {"value": None, "unit": "ms/iter", "cores": 1, "kind": "reference",
-                   "sample": f"failed: {type(exc).__name__}: {exc}"[:300]}
+        cpu = cpu_baseline(args.config)
 
     if rank == 0:
         line = {
@@ -561,8 +726,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded N(0,1) fmaps, Gaussian-smoothed flow drift; "
                     "gen_scenario recipe, fp32 centroids)",
-            "config": {"workload": f"{args.config} {h}x{w} features D={d} L={levels} r={r} "
-                                   f"{n_iter} iterations, one image pair per step",
+            "config": {"workload": workload(args.config),
                        "variant": args.variant, "arith": "strict" if args.strict else "fast",
                        "parallelism": f"query-row bands x{world}" if world > 1 else "1 GPU",
                        "cuda_graph": bool(args.graph),

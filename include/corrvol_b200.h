@@ -262,6 +262,16 @@ int cvb_block_indices(const uint32_t* mask, uint32_t* cum, int64_t rows, int64_t
                       int64_t n_tgt, int64_t used, int64_t* block_ids, int64_t* positions,
                       int64_t max_positions, int64_t* count_out, void* scan_ws, void* stream);
 
+/* Reference-model block accounting for the tile path (the counters
+ * _bench_sparse / run_equivalence read, harness.py:244-245,406-436): with
+ * newly = mask & ~cum (cum treated as empty when reset_cum, the cache-off
+ * reset of sparse.py:426-430), cum |= mask, mask_union |= mask (if non-null),
+ * *total_count += popcount(newly) and *level_count (zeroed first when
+ * reset_cum) += popcount(newly).  Counts are device uint64; no host sync. */
+int cvb_mask_accumulate(const uint32_t* mask, uint32_t* mask_cum, uint32_t* mask_union,
+                        int64_t n_words, int32_t reset_cum, unsigned long long* total_count,
+                        unsigned long long* level_count, void* stream);
+
 /* Sampled block MMM (sampled_block_mmm, sparse.py:312-346): for each of the k
  * positions, the block [B^2, B^2] of dots between source tile s and target
  * tile t, written to store[first_id + i].  f1 / f2l are row-major feature

@@ -11,6 +11,7 @@ exactly like the reference's unknown-backend check (_backend.py:69).
 
 from __future__ import annotations
 
+import functools
 import os
 import types
 from typing import Optional
@@ -42,14 +43,81 @@ def resolve_backend(backend: Optional[str]) -> str:
     return backend
 
 
-def stream_handle() -> int:
-    return torch.cuda.current_stream().cuda_stream
+def stream_handle(device=None) -> int:
+    """cudaStream_t of the current stream of `device` (default: current device).
+
+    Entry points run under `on_device`, which makes the tensors' device the
+    current one, so the library's cudaGetDevice-based choices (shared-memory
+    opt-in, SM count) and this stream always match the data.
+    """
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _device_of(obj):
+    """The CUDA device of a tensor / FeatureMap / CentroidField / state, or None."""
+    if isinstance(obj, torch.Tensor):
+        return obj.device if obj.is_cuda else None
+    if isinstance(obj, (list, tuple)):
+        return _device_of(obj[0]) if obj else None
+    dev = getattr(obj, "device", None)
+    if isinstance(dev, torch.device) and dev.type == "cuda":
+        return dev
+    for attr in ("values", "coords"):
+        t = getattr(obj, attr, None)
+        if isinstance(t, torch.Tensor) and t.is_cuda:
+            return t.device
+    lv = getattr(obj, "levels", None)
+    if isinstance(lv, (list, tuple)) and lv:
+        return _device_of(lv[0])
+    return None
+
+
+class _DeviceGuard:
+    """Make `index` the current CUDA device for the duration (no-op when it is)."""
+
+    __slots__ = ("index", "prev")
+
+    def __init__(self, index):
+        self.index = index
+        self.prev = None
+
+    def __enter__(self):
+        if self.index is not None:
+            cur = torch.cuda.current_device()
+            if cur != self.index:
+                self.prev = cur
+                torch.cuda.set_device(self.index)
+        return self
+
+    def __exit__(self, *exc):
+        if self.prev is not None:
+            torch.cuda.set_device(self.prev)
+        return False
+
+
+def on_device(fn):
+    """Run `fn` with the device of its first CUDA argument current, so kernels
+    launch on that device's current stream (a sampler built on cuda:1 never
+    launches on cuda:0's stream)."""
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        dev = None
+        for a in list(args) + list(kwargs.values()):
+            dev = _device_of(a)
+            if dev is not None:
+                break
+        with _DeviceGuard(None if dev is None else dev.index):
+            return fn(*args, **kwargs)
+
+    return wrapper
 
 
 def _flags(strict: bool) -> int:
     return _lib.CVB_STRICT if strict else 0
 
 
+@on_device
 def corr_pairs(a: torch.Tensor, b: torch.Tensor, strict: bool = False) -> torch.Tensor:
     """[n, D] x [m, D] -> [n, m] float32 dots (_ckernels.pyx:17-32)."""
     require_cuda(a, b)
@@ -63,6 +131,7 @@ def corr_pairs(a: torch.Tensor, b: torch.Tensor, strict: bool = False) -> torch.
     return out
 
 
+@on_device
 def corr_gather(f1: torch.Tensor, f2: torch.Tensor, idx: torch.Tensor, valid: torch.Tensor,
                 strict: bool = False) -> torch.Tensor:
     """out[p] = valid[p] ? dot(f1[p], f2[idx[p]]) : 0 (_ckernels.pyx:35-52)."""
@@ -80,6 +149,7 @@ def corr_gather(f1: torch.Tensor, f2: torch.Tensor, idx: torch.Tensor, valid: to
     return out
 
 
+@on_device
 def block_mmm(at: torch.Tensor, bt: torch.Tensor, strict: bool = False) -> torch.Tensor:
     """[k, n, D] x [k, m, D] -> [k, n, m] (_ckernels.pyx:55-70)."""
     require_cuda(at, bt)
@@ -95,6 +165,7 @@ def block_mmm(at: torch.Tensor, bt: torch.Tensor, strict: bool = False) -> torch
     return out
 
 
+@on_device
 def pool2x2(arr: torch.Tensor) -> torch.Tensor:
     """2x2/stride-2 average pool with floor dims, bit-exact (_pykernels.py:65-81)."""
     require_cuda(arr)

@@ -93,6 +93,7 @@ SIGNATURES = {
     "cvb_resample_flow": (C.c_int, [_p, _i32, _i32, C.c_double, _p, _i32, _i32, _p]),
     "cvb_computation_mask": (C.c_int, [_p, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _p,
                                        _i64, _p]),
+    "cvb_mask_accumulate": (C.c_int, [_p, _p, _p, _i64, _i32, _p, _p, _p]),
     "cvb_block_indices_workspace": (_i64, [_i64]),
     "cvb_block_indices": (C.c_int, [_p, _p, _i64, _i64, _i64, _i64, _p, _p, _i64, _p, _p, _p]),
     "cvb_sampled_block_mmm": (C.c_int, [_p, _i32, _i32, _i32, _p, _i32, _i32, _i32, _i32, _i32,

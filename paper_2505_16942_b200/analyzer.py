@@ -19,7 +19,7 @@ from typing import Dict, List, Sequence, Tuple
 import torch
 
 from . import _lib
-from ._backend import stream_handle
+from ._backend import on_device, stream_handle
 from .dense import coords_flags, pooled_dims
 from .types import CentroidField, LookupSpec
 
@@ -49,6 +49,7 @@ def _groups(shape: Tuple[int, int], block: int, layout: str) -> int:
     raise ValueError(f"layout must be one of {LAYOUTS}, got {layout!r}")
 
 
+@on_device
 def record_occupancy(centroid_fields: Sequence[CentroidField], spec: LookupSpec,
                      tgt_shape: Tuple[int, int], block_sizes: Sequence[int] = (1, 2, 4, 8),
                      layouts: Sequence[str] = LAYOUTS, trim: bool = True) -> List[LevelAccess]:

@@ -205,6 +205,32 @@ __global__ void __launch_bounds__(128)
     o[t] = tap_from_patch<STRICT>(patch, S, t / K, t % K, w64, w32, scale, normalize);
 }
 
+// Reference-model block accounting for the tile path (sparse.py:293-309 and
+// :426-430 without the ids): newly = mask & ~cum (cum cleared first when the
+// cache is off), cum |= mask, union |= mask; the newly bits are added to the
+// run total and to the level's store count.  One warp-reduced atomic per warp.
+__global__ void __launch_bounds__(256)
+    mask_accumulate_kernel(const uint32_t* __restrict__ mask, uint32_t* __restrict__ cum,
+                           uint32_t* __restrict__ uni, int64_t n, bool reset,
+                           unsigned long long* __restrict__ total,
+                           unsigned long long* __restrict__ level_used) {
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t m = mask[i];
+    const uint32_t old = reset ? 0u : cum[i];
+    c += __popc(m & ~old);
+    cum[i] = old | m;
+    if (uni != nullptr) uni[i] |= m;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c != 0) {
+    if (total != nullptr) atomicAdd(total, c);
+    if (level_used != nullptr) atomicAdd(level_used, c);
+  }
+}
+
 }  // namespace cvb
 
 using namespace cvb;
@@ -226,6 +252,20 @@ int cvb_computation_mask(const void* coords, int32_t h1, int32_t w1, int32_t lev
       coords, flags & CVB_COORDS_F64, h1, w1, level, radius, block, pth, ptw, tiles_x_src,
       ptw / block, mask, words_per_row);
   return check_launch("computation_mask");
+}
+
+int cvb_mask_accumulate(const uint32_t* mask, uint32_t* mask_cum, uint32_t* mask_union,
+                        int64_t n_words, int32_t reset_cum, unsigned long long* total_count,
+                        unsigned long long* level_count, void* stream) {
+  CVB_REQUIRE(n_words >= 0, "mask_accumulate: bad size");
+  cudaStream_t s = as_stream(stream);
+  if (reset_cum && level_count != nullptr) cudaMemsetAsync(level_count, 0, sizeof(*level_count), s);
+  if (n_words == 0) return check_launch("mask_accumulate");
+  CVB_REQUIRE(mask && mask_cum, "mask_accumulate: null pointer");
+  const int64_t blocks = ceil_div(n_words, 256);
+  mask_accumulate_kernel<<<(unsigned)(blocks < 148 * 8 ? blocks : 148 * 8), 256, 0, s>>>(
+      mask, mask_cum, mask_union, n_words, reset_cum != 0, total_count, level_count);
+  return check_launch("mask_accumulate");
 }
 
 int64_t cvb_block_indices_workspace(int64_t total_words) {

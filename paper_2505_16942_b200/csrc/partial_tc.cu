@@ -27,6 +27,7 @@
 //     removes the power-of-two scales and writes each cell's 64 query costs
 //     into its cache slot.
 #include <cuda_fp16.h>
+#include <stddef.h>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -214,8 +215,9 @@ struct TcParams {
   const int8_t* e2[CVB_MAX_LEVELS];    // per cell exponent
   int64_t plane[CVB_MAX_LEVELS];
   int dp;
-  int dbg;                             // profiling knockouts (CVB_TC_DEBUG), 0 in production
-  unsigned long long* ts;              // role timeline (CVB_TC_DEBUG & 16), null in production
+  int dbg;                             // profiling knockouts (CVB_TC_DEBUG; debug instantiation only)
+  unsigned long long* ts;              // role timeline (CVB_TC_DEBUG & 16; debug instantiation only)
+  int* watchdog;                       // host-mapped error word (null: none); see wait_phase
 };
 
 // Operand preparation, once per image pair.  Every row (a query of F1, a
@@ -451,7 +453,13 @@ constexpr int NPL = 4;              // plan slots
 constexpr int THREADS = 512;
 constexpr int A_WARPS = 8;             // A producers: warps 4-7 and 12-15
 constexpr int A_ROWS = 128 / A_WARPS;  // A rows per producer warp
-constexpr uint32_t SPIN_LIMIT = 1u << 24;  // watchdog: trap instead of hanging
+// Pipeline watchdog: a ring wait that has not completed after this long
+// (%globaltimer ns) means a broken pipeline, not a slow one.  The CTA then sets
+// its abort flag, every role leaves its loop at its next wait, the kernel exits
+// normally and the host-mapped error word makes the NEXT contraction call
+// return CVB_ERR_CUDA.  (The CUDA context survives, unlike with __trap().)
+constexpr unsigned long long WATCHDOG_NS = 20ull * 1000 * 1000 * 1000;
+constexpr int WATCHDOG_CODE = 0x5744;  // 'WD'
 
 struct Ctl {
   uint64_t plan_full[NPL], plan_empty[NPL];
@@ -461,6 +469,7 @@ struct Ctl {
   PlanRec slot[NPL];
   float qscale[tc::N];
   uint32_t tmem;
+  int abort;  // watchdog fired in this CTA
 };
 
 __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
@@ -474,36 +483,63 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Wait for `parity` on `bar`; false if the CTA's pipeline was aborted.  The
+// fast path is one try_wait; the clock is read only every 64 failed polls.
+__device__ __noinline__ bool wait_slow(uint32_t bar, uint32_t parity, volatile int* abort,
+                                       int* word) {
+  const unsigned long long t0 = global_ns();
+  for (uint32_t n = 1;; ++n) {
+    if (mbar_try(bar, parity)) return true;
+    if ((n & 63u) == 0) {
+      if (*abort) return false;
+      if (global_ns() - t0 > WATCHDOG_NS) {
+        *abort = 1;
+        if (word != nullptr) atomicExch_system(word, WATCHDOG_CODE);
+        return false;
+      }
+    }
+  }
+}
+__device__ __forceinline__ bool wait_phase(uint32_t bar, uint32_t parity, volatile int* abort,
+                                           int* word) {
+  return mbar_try(bar, parity) || wait_slow(bar, parity, abort, word);
+}
 // full barriers: the k-th completion has parity k&1; empty barriers: the
 // producer's k-th wait passes on parity (k&1)^1 (a fresh barrier counts as
 // having completed the phase before phase 0).
-__device__ __forceinline__ void wait_full(uint32_t bar, uint32_t k) {
-  for (uint32_t n = 0; !mbar_try(bar, k & 1u); ++n)
-    if (n > SPIN_LIMIT) __trap();
-}
-__device__ __forceinline__ void wait_empty(uint32_t bar, uint32_t k) {
-  for (uint32_t n = 0; !mbar_try(bar, (k & 1u) ^ 1u); ++n)
-    if (n > SPIN_LIMIT) __trap();
-}
+#define WAIT_FULL(bar, k) wait_phase((bar), (uint32_t)(k) & 1u, &C.abort, T.watchdog)
+#define WAIT_EMPTY(bar, k) wait_phase((bar), ((uint32_t)(k) & 1u) ^ 1u, &C.abort, T.watchdog)
 __device__ __forceinline__ void arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
 // Work counter of the persistent contraction: the plan loader of every CTA
-// claims the next tile with one atomicAdd (dynamic load balance); it lives in
-// the spare record after the n_tiles plan records and is reset by plan_kernel.
+// claims the next tile with one atomicAdd (dynamic load balance).  It is the
+// `pad` word of the range's FIRST plan record, which belongs to this range
+// alone (ranges are disjoint), so contractions of disjoint tile ranges may run
+// concurrently on different streams (include/corrvol_b200.h).  plan_kernel
+// resets it; the contraction's pdl_wait orders the reset before the claims.
 __device__ __forceinline__ int* tile_counter(const PartialParams& P) {
-  return P.plans + P.n_tiles * PLAN_INTS;
+  return P.plans + P.tile0 * PLAN_INTS + (int)(offsetof(PlanRec, pad) / 4);
 }
 
+template <bool DEBUG>
 __device__ __forceinline__ void stamp(const tc::TcParams& T, int64_t it, int e) {
-  if (T.ts != nullptr && blockIdx.x < 4 && it < 64) {
+  if (DEBUG && T.ts != nullptr && blockIdx.x < 4 && it < 64) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     T.ts[((int64_t)blockIdx.x * 64 + it) * 32 + e] = t;
   }
 }
 
+// DEBUG=false is the production instantiation: the CVB_TC_DEBUG knock-outs
+// and the %globaltimer role timeline compile out of it.
+template <bool DEBUG>
 __global__ void __launch_bounds__(THREADS, 1)
     partial_contract_tcp_kernel(const __grid_constant__ tc::TcParams T) {
   extern __shared__ uint8_t smem_raw[];
@@ -543,6 +579,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_init(U(C.acc_full[i]), 1);
       tc::mbar_init(U(C.acc_empty[i]), 128);
     }
+    C.abort = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   tc::tc_fence_before();
@@ -558,16 +595,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t pb = 0;  // pieces issued so far
       for (int64_t it = 0;; ++it) {
         const int s = (int)(it % NPL);
-        wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
+        if (!WAIT_FULL(U(C.plan_full[s]), (uint32_t)(it / NPL))) goto done;
         const int tile_i = C.slot[s].tile;
         if (tile_i < 0) break;
         if (C.slot[s].n_cells > 0) {
           const uint8_t* src = T.f1s + (int64_t)tile_i * n_kb * tc::B_PIECE;
           for (int q = 0; q < n_kb; ++q, ++pb) {
             const int bs = (int)(pb % NBP);
-            wait_empty(U(C.b_empty[bs]), pb / NBP);
-            stamp(T, it, 24 + q);
-            if (T.dbg & 8) {
+            if (!WAIT_EMPTY(U(C.b_empty[bs]), pb / NBP)) goto done;
+            stamp<DEBUG>(T, it, 24 + q);
+            if (DEBUG && (T.dbg & 8)) {
               arrive(U(C.b_full[bs]));
               continue;
             }
@@ -576,7 +613,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                          U(C.b_full[bs]));
           }
         }
-        stamp(T, it, 5);
+        stamp<DEBUG>(T, it, 5);
         arrive(U(C.plan_empty[s]));
       }
     }
@@ -589,35 +626,35 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t pb = 0, g = 0, cg = 0;
     for (int64_t it = 0;; ++it) {
       const int s = (int)(it % NPL);
-      wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
+      if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.plan_full[s]), (uint32_t)(it / NPL)))) goto done;
       if (C.slot[s].tile < 0) break;
-      if (lane == 0) stamp(T, it, 1);
+      if (lane == 0) stamp<DEBUG>(T, it, 1);
       const int n = C.slot[s].n_cells;
       if (n > 0) {
         const int n_chunks = (n + tc::M - 1) / tc::M;
         for (int c = 0; c < n_chunks; ++c, ++cg) {
           const int ab = cg & 1;
-          wait_empty(U(C.acc_empty[ab]), cg >> 1);
+          if (!__all_sync(0xffffffffu, WAIT_EMPTY(U(C.acc_empty[ab]), cg >> 1))) goto done;
           tc::tc_fence_after();
-          if (c == 0 && lane == 0) stamp(T, it, 6);
+          if (c == 0 && lane == 0) stamp<DEBUG>(T, it, 6);
           const uint32_t d_main = tmem + ab * 128, d_corr = d_main + 64;
           for (int kb = 0; kb < n_kb; ++kb, ++g) {
             const uint32_t pi = pb + kb;
             const int bs = (int)(pi % NBP);
             if (c == 0) {
-              wait_full(U(C.b_full[bs]), pi / NBP);
-              if (lane == 0) stamp(T, it, 12 + kb);
+              if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.b_full[bs]), pi / NBP))) goto done;
+              if (lane == 0) stamp<DEBUG>(T, it, 12 + kb);
             }
             const int st = (int)(g % NST);
-            wait_full(U(C.a_full[st]), g / NST);
+            if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.a_full[st]), g / NST))) goto done;
             tc::tc_fence_after();
-            if (c == 0 && lane == 0) stamp(T, it, 8 + kb);
+            if (c == 0 && lane == 0) stamp<DEBUG>(T, it, 8 + kb);
             const uint32_t a_hi = uA + st * tc::A_STAGE, a_lo = a_hi + tc::A_HALF;
             const uint32_t b_hi = uB + bs * tc::B_PIECE;  // hi rows 0-63, lo rows 64-127
             const uint64_t dah = tc::make_desc_sw128(a_hi), dal = tc::make_desc_sw128(a_lo);
             const uint64_t dbh = tc::make_desc(b_hi, 128, (tc::KP / 8) * 128);
             if (tc::elect_one()) {
-              if (!(T.dbg & 4)) {
+              if (!(DEBUG && (T.dbg & 4))) {
 #pragma unroll
                 for (int k = 0; k < tc::KP / 16; ++k) {
                   const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
@@ -636,7 +673,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         pb += n_kb;
       }
       if (lane == 0) {
-        stamp(T, it, 2);
+        stamp<DEBUG>(T, it, 2);
         arrive(U(C.plan_empty[s]));
       }
     }
@@ -645,7 +682,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       for (int64_t it = 0;; ++it) {
         const int s = (int)(it % NPL);
-        wait_empty(U(C.plan_empty[s]), (uint32_t)(it / NPL));
+        if (!WAIT_EMPTY(U(C.plan_empty[s]), (uint32_t)(it / NPL))) goto done;
         const int64_t t = atomicAdd(tile_counter(P), 1);  // dynamic tile scheduler
         if (t >= P.ntile) {  // end of the work list: a sentinel record
           C.slot[s].tile = -1;
@@ -655,7 +692,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::mbar_expect_tx(U(C.plan_full[s]), (uint32_t)sizeof(PlanRec));
         tc::bulk_g2s(tc::smem_u32(&C.slot[s]), P.plans + (P.tile0 + t) * PLAN_INTS,
                      (uint32_t)sizeof(PlanRec), U(C.plan_full[s]));
-        stamp(T, it, 0);
+        stamp<DEBUG>(T, it, 0);
       }
     }
   } else if ((warp >= 4 && warp < 8) || warp >= 12) {
@@ -672,7 +709,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t g = 0;  // A stages issued
     for (int64_t it = 0;; ++it) {
       const int s = (int)(it % NPL);
-      wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
+      if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.plan_full[s]), (uint32_t)(it / NPL)))) goto done;
       const PlanRec& S = C.slot[s];
       if (S.tile < 0) break;
       const int n = S.n_cells;
@@ -689,9 +726,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (int kb = 0; kb < n_kb; ++kb, ++g) {
           const int st = (int)(g % NST);
-          wait_empty(U(C.a_empty[st]), g / NST);
-          if (c == 0 && tid == 128) stamp(T, it, 16 + kb);
-          if (!(T.dbg & 1)) {
+          if (!__all_sync(0xffffffffu, WAIT_EMPTY(U(C.a_empty[st]), g / NST))) goto done;
+          if (c == 0 && tid == 128) stamp<DEBUG>(T, it, 16 + kb);
+          if (!(DEBUG && (T.dbg & 1))) {
             const uint32_t stage = uA + st * tc::A_STAGE;
 #pragma unroll
             for (int i = 0; i < A_ROWS / 4; ++i) {
@@ -715,7 +752,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
-      if (tid == 128) stamp(T, it, 3);
+      if (tid == 128) stamp<DEBUG>(T, it, 3);
       arrive(U(C.plan_empty[s]));
     }
   } else if (warp >= 8 && warp < 12) {
@@ -726,7 +763,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t cg = 0;
     for (int64_t it = 0;; ++it) {
       const int s = (int)(it % NPL);
-      wait_full(U(C.plan_full[s]), (uint32_t)(it / NPL));
+      if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.plan_full[s]), (uint32_t)(it / NPL)))) goto done;
       const PlanRec& S = C.slot[s];
       if (S.tile < 0) break;
       const int64_t tile = S.tile;
@@ -754,16 +791,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                 (int64_t)slot_of(cr.cy, cr.cx, ch, cw) * TQW;
           e_c = T.e2[cr.level][(int64_t)cr.cy * P.tw[cr.level] + cr.cx];
         }
-        wait_full(U(C.acc_full[ab]), cg >> 1);
+        if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.acc_full[ab]), cg >> 1))) goto done;
         tc::tc_fence_after();
-        if (c == 0 && tid == 256) stamp(T, it, 20);
+        if (c == 0 && tid == 256) stamp<DEBUG>(T, it, 20);
         const float s_c = tc::exp2_neg(e_c);
         float vm[32], vc[32];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           tc::tmem_ld32(tmem + ab * 128 + lane_base + h * 32, vm);
           tc::tmem_ld32(tmem + ab * 128 + 64 + lane_base + h * 32, vc);
-          if (dst != nullptr && !(T.dbg & 2)) {
+          if (dst != nullptr && !(DEBUG && (T.dbg & 2))) {
             // this half holds tile rows 4h..4h+3 = query groups 4h/2*2 .. +3;
             // each group's 8 costs (32 B, one cache sector) leave in one
             // 256-bit store, so a warp writes whole sectors of consecutive slots
@@ -786,13 +823,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
         tc::tc_fence_before();
-        if (c == 0 && tid == 256) stamp(T, it, 21);
+        if (c == 0 && tid == 256) stamp<DEBUG>(T, it, 21);
         arrive(U(C.acc_empty[ab]));
       }
-      if (tid == 256) stamp(T, it, 4);
+      if (tid == 256) stamp<DEBUG>(T, it, 4);
       arrive(U(C.plan_empty[s]));
     }
   }
+done:  // normal exit, or a role leaving early after the watchdog fired
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -935,6 +973,56 @@ size_t smem_bytes() {
   return (size_t)NST * tc::A_STAGE + (size_t)NBP * tc::B_PIECE + sizeof(Ctl) + 1024;
 }
 
+// SM count per device (the persistent grid size), queried once per device.
+int sm_count(int dev) {
+  static std::atomic<int> cache[64];
+  if (dev < 0 || dev >= 64) dev = 0;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+
+// The watchdog's error word: one int of portable, host-mapped pinned memory
+// (the kernel writes it with a system-scope atomic; the host reads it on the
+// next call without a synchronisation).  Allocated on the first call that is
+// not being captured into a CUDA graph; null until then (no reporting).
+int* watchdog_host = nullptr;
+int* watchdog_dev = nullptr;
+int* watchdog_word(cudaStream_t s) {
+  static std::atomic<int> state{0};  // 0 unallocated, 1 ready, 2 failed
+  if (state.load(std::memory_order_acquire) == 0) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    static std::atomic_flag lock = ATOMIC_FLAG_INIT;
+    while (lock.test_and_set(std::memory_order_acquire)) {
+    }
+    if (state.load() == 0) {
+      void* h = nullptr;
+      void* d = nullptr;
+      if (cudaHostAlloc(&h, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable) ==
+              cudaSuccess &&
+          cudaHostGetDevicePointer(&d, h, 0) == cudaSuccess) {
+        *(volatile int*)h = 0;
+        watchdog_host = (int*)h;
+        watchdog_dev = (int*)d;
+        state.store(1, std::memory_order_release);
+      } else {
+        cudaGetLastError();
+        state.store(2, std::memory_order_release);
+      }
+    }
+    lock.clear(std::memory_order_release);
+  }
+  return state.load(std::memory_order_acquire) == 1 ? watchdog_host : nullptr;
+}
+
 }  // namespace tcp
 
 }  // namespace cvb
@@ -1045,9 +1133,21 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
     T.e2[l] = used ? reinterpret_cast<const int8_t*>(T.f2s[l] + 2 * T.plane[l]) : nullptr;
     if (used) CVB_REQUIRE(T.f2s[l], "partial_contract_tc: null level pointer");
   }
+  // a watchdog abort of an earlier launch (its outputs are invalid) surfaces here
+  int* word = tcp::watchdog_word(as_stream(stream));
+  if (word != nullptr && *(volatile int*)word != 0) {
+    *(volatile int*)word = 0;
+    set_error("partial_contract_tc: a previous contraction launch was aborted by its pipeline "
+              "watchdog (a ring wait exceeded %llu s); its cache and outputs are invalid",
+              tcp::WATCHDOG_NS / 1000000000ull);
+    return CVB_ERR_CUDA;
+  }
+  T.watchdog = word != nullptr ? tcp::watchdog_dev : nullptr;
   if (T.P.ntile == 0) return CVB_OK;
-  static int n_sms = 0;  // 148 on every B200
-  static int dbg = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int n_sms = tcp::sm_count(dev);
+  static int dbg = -1;  // CVB_TC_DEBUG: profiling knock-outs / timeline (debug kernel)
   if (dbg < 0) {
     const char* e = getenv("CVB_TC_DEBUG");
     dbg = e ? atoi(e) : 0;
@@ -1060,20 +1160,15 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
     cudaMemsetAsync(ts_buf, 0, 4 * 64 * 32 * sizeof(unsigned long long), as_stream(stream));
     T.ts = ts_buf;
   }
-  if (n_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
   const size_t smem = tcp::smem_bytes();
-  static std::atomic<uint64_t> attr{0};
-  ensure_max_smem(attr, tcp::partial_contract_tcp_kernel, (int)smem);
+  auto kernel = dbg ? tcp::partial_contract_tcp_kernel<true> : tcp::partial_contract_tcp_kernel<false>;
+  static std::atomic<uint64_t> attr_prod{0}, attr_dbg{0};
+  ensure_max_smem(dbg ? attr_dbg : attr_prod, kernel, (int)smem);
   launch_pdl(tcp::plan_kernel, dim3((unsigned)ceil_div(T.P.ntile, tcp::PLAN_WARPS)),
              dim3(tcp::PLAN_WARPS * 32), 0, as_stream(stream), T.P);
   if ((st = check_launch("partial_plan")) != CVB_OK) return st;
   const int64_t grid = T.P.ntile < n_sms ? T.P.ntile : n_sms;
-  launch_pdl(tcp::partial_contract_tcp_kernel, dim3((unsigned)grid), dim3(tcp::THREADS), smem,
-             as_stream(stream), T);
+  launch_pdl(kernel, dim3((unsigned)grid), dim3(tcp::THREADS), smem, as_stream(stream), T);
   if (T.ts != nullptr) {  // debug timeline dump (CTA 0..3, first 64 tiles, 32 events), ns
     static unsigned long long h[4 * 64 * 32];
     cudaStreamSynchronize(as_stream(stream));

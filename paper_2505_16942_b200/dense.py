@@ -14,7 +14,7 @@ from typing import List, Optional, Tuple
 import torch
 
 from . import _lib
-from ._backend import resolve_backend, stream_handle
+from ._backend import on_device, resolve_backend, stream_handle
 from .types import (CentroidField, CostMaps, FeatureMap, FeaturePyramid, LookupSpec,
                     WorkCounter, require_cuda)
 
@@ -47,6 +47,7 @@ def alloc_feature_pyramid(f2: FeatureMap, levels: int) -> FeaturePyramid:
     return FeaturePyramid(levels=maps)
 
 
+@on_device
 def build_feature_pyramid(f2: FeatureMap, levels: int) -> FeaturePyramid:
     """L-level pyramid of f2 (dense.py:71-86)."""
     pyr = alloc_feature_pyramid(f2, levels)
@@ -56,6 +57,7 @@ def build_feature_pyramid(f2: FeatureMap, levels: int) -> FeaturePyramid:
     return pyr
 
 
+@on_device
 def build_dense_volume(f1: FeatureMap, f2: FeatureMap, backend: Optional[str] = None,
                        counter: Optional[WorkCounter] = None, strict: bool = False
                        ) -> torch.Tensor:
@@ -73,6 +75,7 @@ def build_dense_volume(f1: FeatureMap, f2: FeatureMap, backend: Optional[str] = 
     return out
 
 
+@on_device
 def pool_volume(mat: torch.Tensor, tgt_shape: Tuple[int, int]) -> torch.Tensor:
     """2x2 pooling of the volume's target dims (dense.py:48-60)."""
     th, tw = tgt_shape
@@ -117,6 +120,7 @@ def estimate_dense_bytes(src_shape: Tuple[int, int], tgt_shape: Tuple[int, int],
     return total
 
 
+@on_device
 def build_volume_pyramid(f1: FeatureMap, f2: FeatureMap, levels: int, mode: str = "pool_volume",
                          backend: Optional[str] = None, counter: Optional[WorkCounter] = None,
                          strict: bool = False) -> DenseCorrelationVolume:
@@ -149,6 +153,7 @@ def coords_flags(centroids: CentroidField, strict: bool) -> int:
     return f | (_lib.CVB_STRICT if strict else 0)
 
 
+@on_device
 def lookup_dense(vol: DenseCorrelationVolume, centroids: CentroidField, spec: LookupSpec,
                  strict: bool = False, out: Optional[torch.Tensor] = None) -> CostMaps:
     """Bilinear (2r+1)^2 windows from the dense volume (dense.py:188-223)."""

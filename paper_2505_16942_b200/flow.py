@@ -12,10 +12,11 @@ import math
 import torch
 
 from . import _lib
-from ._backend import stream_handle
+from ._backend import on_device, stream_handle
 from .types import require_cuda
 
 
+@on_device
 def resample_flow(vectors: torch.Tensor, scale: float) -> torch.Tensor:
     """Bilinearly resample a [H, W, 2] float32 flow field to round(dim*scale)
     (half-up) dims with edge clamping, magnitudes multiplied by scale."""

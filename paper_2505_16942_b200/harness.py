@@ -154,7 +154,8 @@ def _bench_sparse(s: _Scn, block: int, cache_enabled: bool, strict: bool,
     common = _common(s, "sparse" if mode == "block" else "partial", block,
                      "on" if cache_enabled else "off")
     return BenchRecord(dot_products=cnt.dot_products, macs=cnt.macs,
-                       blocks_computed=cnt.blocks_computed, blocks_stored=stored,
+                       blocks_computed=cnt.blocks_computed if mode == "block" else 0,
+                       blocks_stored=stored,
                        blocks_union=union, block_positions=positions, peak_bytes=max(peaks),
                        wall_ms=ms, shares=None, oom=False, **common)
 

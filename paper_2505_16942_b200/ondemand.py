@@ -16,12 +16,13 @@ from typing import Optional, Sequence, Tuple
 import torch
 
 from . import _lib
-from ._backend import resolve_backend, stream_handle
+from ._backend import on_device, resolve_backend, stream_handle
 from .dense import coords_flags, pooled_dims
 from .types import (CentroidField, CostMaps, FeatureMap, FeaturePyramid, LookupSpec,
                     WorkCounter, require_cuda)
 
 
+@on_device
 def lookup_on_demand(f1: FeatureMap, pyr: FeaturePyramid, centroids: CentroidField,
                      spec: LookupSpec, backend: Optional[str] = None,
                      counter: Optional[WorkCounter] = None, strict: bool = False,

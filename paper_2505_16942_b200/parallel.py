@@ -67,8 +67,10 @@ def gather_bands(local: torch.Tensor, bands: Sequence[Tuple[int, int]],
         full = torch.empty((world * rows,) + tail, dtype=local.dtype, device=local.device)
         dist.all_gather_into_tensor(full, buf, group=group)
         chunks = [full[r * rows: (r + 1) * rows] for r in range(world)]
-    else:  # gloo (CPU tests): list all_gather
-        chunks = [torch.empty_like(buf) for _ in range(world)]
-        dist.all_gather(chunks, buf, group=group)
+    else:  # gloo (CPU tests; ranks sharing one GPU): list all_gather on the host
+        host = buf.cpu()
+        chunks = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(chunks, host, group=group)
+        chunks = [c.to(local.device) for c in chunks]
     parts = [chunks[r][: b - a] for r, (a, b) in enumerate(bands)]
     return torch.cat(parts, dim=0)

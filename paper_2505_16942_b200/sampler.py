@@ -47,7 +47,11 @@ class CorrSampler:
         # launch sequence (tiler, contraction, sampler) is replayed from a
         # captured CUDA graph on static coordinate / output buffers — for
         # launch-bound frames; the returned tensor is reused by the next call
-        self.graph = graph and variant == "partial"
+        if graph and (variant != "partial" or mode != "tile"):
+            # block mode sizes its store on the host (.item() syncs, host-side
+            # growth): nothing a replayed graph could reproduce
+            raise ValueError("graph=True needs variant='partial' with mode='tile'")
+        self.graph = graph
         self._graph = None
         self._g_coords = None
         self._g_out = None
@@ -150,6 +154,10 @@ class BatchCorrSampler:
 
     def __len__(self) -> int:
         return len(self.samplers)
+
+    def states(self):
+        """Per-pair partial-sampler states (device counters, footprints)."""
+        return [s.state for s in self.samplers]
 
     def __call__(self, coords: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         b, h, w = coords.shape[:3]

@@ -30,7 +30,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._backend import resolve_backend, stream_handle
+from ._backend import on_device, resolve_backend, stream_handle
 from .dense import alloc_feature_pyramid, build_feature_pyramid, coords_flags, pooled_dims
 from .types import (CacheLimitError, CentroidField, CostMaps, FeatureMap, FeaturePyramid,
                     GatherMissError, LookupSpec, WorkCounter, require_cuda)
@@ -168,6 +168,37 @@ class BlockStore:
         self.used = 0
 
 
+class _StoreCount:
+    """Tile mode with ref_counters: the `store.used` the reference's BlockStore
+    would report (blocks of the level held after this iteration), kept on the
+    device and synced when read."""
+
+    def __init__(self, counts: torch.Tensor, index: int, bytes_per_block: int):
+        self._counts = counts
+        self._index = index
+        self.bytes_per_block = bytes_per_block
+
+    @property
+    def used(self) -> int:
+        return int(self._counts[self._index].item())
+
+    def used_bytes(self) -> int:
+        return self.used * self.bytes_per_block
+
+
+class TileWorkCounter(WorkCounter):
+    """WorkCounter of a tile-mode state without ref_counters: dot_products /
+    macs are the tile path's executed dots; the reference's block currency is
+    not tracked, and reading it fails loudly instead of returning 0."""
+
+    def __getattribute__(self, name):
+        if name == "blocks_computed":
+            raise RuntimeError(
+                "blocks_computed is the reference's block-granular work currency; the tile "
+                "path tracks it only with init_state(..., ref_counters=True)")
+        return super().__getattribute__(name)
+
+
 _POPC = None
 
 
@@ -259,6 +290,8 @@ class SparseVolumeState:
         self.n_tiles = 0
         self.tc_f1 = None
         self.tc_f2 = None
+        self.ref_counters = False
+        self._ref_counts = None
 
     # -- reference-compatible attributes ------------------------------------
     @property
@@ -282,11 +315,25 @@ class SparseVolumeState:
 
     @property
     def counter(self) -> WorkCounter:
-        """WorkCounter synced from the device (one sync per read)."""
+        """WorkCounter synced from the device (one sync per read).
+
+        Tile mode with ref_counters: the reference's block-model counts
+        (blocks_computed; dot_products = blocks * B^4, sparse.py:342-346).
+        Tile mode without: the tile path's executed dots, and blocks_computed
+        raises (TileWorkCounter)."""
         if self.mode == "tile":
+            if self.ref_counters:
+                blocks = int(self._ref_counts[0].item())
+                b4 = self.block ** 4
+                self._counter.blocks_computed = blocks
+                self._counter.dot_products = blocks * b4
+                self._counter.macs = blocks * b4 * self.f1.dims
+                return self._counter
             dots = int(self._dev_counters[0].item())
-            self._counter.dot_products = dots
-            self._counter.macs = dots * self.f1.dims
+            c = TileWorkCounter()
+            c.dot_products = dots
+            c.macs = dots * self.f1.dims
+            return c
         return self._counter
 
     @property
@@ -310,13 +357,15 @@ def _tile_caps(spec: LookupSpec, tile_caps) -> List[Tuple[int, int]]:
     return caps
 
 
+@on_device
 def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
                cache_cap_bytes: Optional[int] = None, hard_limit_bytes: Optional[int] = None,
                growth_factor: int = 2, cache_enabled: bool = True,
                backend: Optional[str] = None, mode: str = "tile", strict: bool = False,
                tile_caps=None, pyramid: Optional[FeaturePyramid] = None,
                tensor_cores: Optional[bool] = None,
-               pipeline_splits: Optional[int] = None) -> SparseVolumeState:
+               pipeline_splits: Optional[int] = None,
+               ref_counters: bool = False) -> SparseVolumeState:
     """One-time preprocessing for an image pair (sparse.py:205-248).
 
     Builds the fmap2 pyramid on the GPU and allocates the level states.
@@ -325,6 +374,12 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
     mode="block": reference block store per level (growth, cap, hard limit).
     tensor_cores (tile mode, fast arithmetic): contract on tcgen05 with
     split-fp16 operands (default when not strict and D <= 256).
+    ref_counters (tile mode): also keep the reference's block-granular state
+    per iteration on the device — bit-packed mask_cum / mask_union and the
+    block counts (counter.blocks_computed, levels[l].store.used,
+    mask_union, block_positions) that the reference harness reads
+    (harness.py:244-245,406-436) — at one mask kernel + one accumulate kernel
+    per level and iteration; off by default so the timed path is not taxed.
     """
     resolve_backend(backend)
     if f1.dims != f2.dims:
@@ -384,6 +439,14 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
             lv.cache = torch.empty(per_level[lvl], dtype=torch.float32, device=dev)
         _lib.call("cvb_partial_reset", _lib.C.byref(desc), _lib.ptr(state.meta),
                   stream_handle())
+        if ref_counters:
+            state.ref_counters = True
+            state._ref_counts = torch.zeros(1 + spec.levels, dtype=torch.int64, device=dev)
+            for lvl, lv in enumerate(levels):
+                n_src, wpr = pm1.n_tiles, lv.words_per_row
+                lv.mask_cum_bits = torch.zeros((n_src, wpr), dtype=torch.int32, device=dev)
+                lv.mask_union_bits = torch.zeros((n_src, wpr), dtype=torch.int32, device=dev)
+                lv.store = _StoreCount(state._ref_counts, 1 + lvl, 4 * block ** 4)
         if tensor_cores:
             _prepare_tc(state, pool=fuse_pyramid)
             # overlap contraction and gathering across tile ranges when the frame
@@ -482,6 +545,7 @@ def _mask_bits(state: SparseVolumeState, centroids: CentroidField, level: int) -
     return mask
 
 
+@on_device
 def set_computation_mask(state: SparseVolumeState, centroids: CentroidField,
                          level: int) -> torch.Tensor:
     """This iteration's [n_src_tiles, n_tgt_tiles] bool mask (sparse.py:262-290); pure."""
@@ -520,6 +584,7 @@ def _block_indices_bits(state: SparseVolumeState, mask_bits: torch.Tensor, level
     return positions[:k], ids
 
 
+@on_device
 def compute_block_indices(state: SparseVolumeState, new_mask: torch.Tensor, level: int):
     """Assign ids to this iteration's newly needed blocks (sparse.py:293-309)."""
     lv = state.levels[level]
@@ -527,6 +592,7 @@ def compute_block_indices(state: SparseVolumeState, new_mask: torch.Tensor, leve
                                level)
 
 
+@on_device
 def sampled_block_mmm(state: SparseVolumeState, level: int, positions: torch.Tensor,
                       timings=None) -> torch.Tensor:
     """Compute and append the blocks at `positions` (sparse.py:312-346)."""
@@ -615,6 +681,18 @@ def _sample_block_mode(state: SparseVolumeState, centroids: CentroidField,
         raise GatherMissError("a proxy gather hit a block that was never computed")
 
 
+def _accumulate_ref_counters(state: SparseVolumeState, centroids: CentroidField) -> None:
+    """The reference's mask / block accounting for one tile-mode iteration
+    (set_computation_mask + the counting half of compute_block_indices,
+    sparse.py:262-309, with the cache-off reset of :426-430), on the device."""
+    counts = state._ref_counts
+    for lvl, lv in enumerate(state.levels):
+        mask = _mask_bits(state, centroids, lvl)
+        _lib.call("cvb_mask_accumulate", _lib.ptr(mask), _lib.ptr(lv.mask_cum_bits),
+                  _lib.ptr(lv.mask_union_bits), mask.numel(), 0 if state.cache_enabled else 1,
+                  _lib.ptr(counts), counts.data_ptr() + 8 * (1 + lvl), stream_handle())
+
+
 def _range_descs(state: SparseVolumeState, splits: int):
     """PartialDesc copies covering `splits` contiguous tile ranges."""
     key = ("ranges", splits)
@@ -671,6 +749,7 @@ def _sample_tile_mode(state: SparseVolumeState, centroids: CentroidField,
     main.wait_event(ev)
 
 
+@on_device
 def sample_iteration(state: SparseVolumeState, centroids: CentroidField,
                      out: Optional[torch.Tensor] = None) -> CostMaps:
     """One lookup iteration (sparse.py:411-452); returns [H, W, L, 2r+1, 2r+1]."""
@@ -682,12 +761,15 @@ def sample_iteration(state: SparseVolumeState, centroids: CentroidField,
                           device=state.device)
     if state.mode == "tile":
         _sample_tile_mode(state, centroids, out)
+        if state.ref_counters:
+            _accumulate_ref_counters(state, centroids)
     else:
         _sample_block_mode(state, centroids, out)
     state.iteration += 1
     return CostMaps(values=out, radius=spec.radius)
 
 
+@on_device
 def sample_iteration_raft(state: SparseVolumeState, centroids: CentroidField,
                           out: torch.Tensor) -> torch.Tensor:
     """One lookup iteration written straight into RAFT's CorrBlock layout:
@@ -739,19 +821,24 @@ def memory_footprint(state: SparseVolumeState) -> Dict:
         per_level.append({"level": lvl, "mask_bytes": mask_bytes, "block_bytes": block_bytes,
                           "capacity_bytes": cap_bytes, "feature_bytes": fbytes_all,
                           "blocks_used": blocks_used,
-                          "block_positions": lv.block_positions if state.mode == "block" else 0})
+                          "block_positions": lv.block_positions})
         mask_total += mask_bytes
         used_total += block_bytes
         cap_total += cap_bytes
         feat_total += fbytes
         blocks_used_total += blocks_used
     feat_total += state.pyramid.levels[0].values.numel() * 4
+    # tensor-core path: the fp16 hi/lo operand planes of F1 and of every level
+    split_total = 0
+    if state.tc:
+        split_total = state.tc_f1.numel() + sum(t.numel() for t in state.tc_f2)
     return {"levels": per_level, "mask_bytes": mask_total, "block_bytes": used_total,
             "capacity_bytes": cap_total, "feature_bytes": feat_total,
-            "blocks_used": blocks_used_total,
-            "total_bytes": mask_total + cap_total + feat_total}
+            "split_bytes": split_total, "blocks_used": blocks_used_total,
+            "total_bytes": mask_total + cap_total + feat_total + split_total}
 
 
+@on_device
 def sample_iteration_timed(state: SparseVolumeState, centroids: CentroidField,
                            out: torch.Tensor) -> Tuple[torch.cuda.Event, ...]:
     """Tile-mode iteration with CUDA events around each kernel (bench helper).
