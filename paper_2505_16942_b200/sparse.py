@@ -44,8 +44,11 @@ MODES = ("tile", "block")
 #: Default toroidal cache window (cells per axis) per level for 8x8 query tiles.
 #: An 8x8 tile's support box is >= (8/2^l + 2r+1) cells per axis; the window
 #: leaves room for flow divergence.  Boxes that do not fit are evaluated
-#: directly for that iteration (never wrong, only slower).
-DEFAULT_TILE_CAPS = (32, 20, 16, 16, 16, 16, 16, 16)
+#: directly for that iteration (never wrong, only slower).  34/22 hold the
+#: largest box of every BASELINE workload (C1-C4 seed 0 and C5 seeds 0-7;
+#: widest: C5 seed 7, 33x33 at level 0, 21x21 at level 1); levels >= 2 get
+#: the 2r+2+8 floor (18 at r=4).
+DEFAULT_TILE_CAPS = (34, 22, 16, 16, 16, 16, 16, 16)
 
 
 def _default_cache_cap() -> int:
