@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define CVB_ABI_VERSION 1
+#define CVB_ABI_VERSION 2
 
 typedef enum {
   CVB_OK = 0,
@@ -160,6 +160,12 @@ typedef struct {
    * ranges may run concurrently; gather(range) depends only on
    * contract(range) of the same iteration. */
   int32_t tile_begin, tile_end;
+  /* image pairs of equal geometry processed by every launch (0 or 1: one).
+   * Batched buffers are pair-major: f1 / coords / the cost map are
+   * [batch, h1, w1, ...], level maps [batch, th, tw, d]; tiles of pair b are
+   * [b*tiles, (b+1)*tiles) and meta / plans / cache / split operands are
+   * sized for all of them (the *_sizes queries include the batch). */
+  int32_t batch;
 } cvb_partial_desc;
 
 /* tiles = ceil(h1/8)*ceil(w1/8); meta is int32 [tiles, levels, 8]; cache for

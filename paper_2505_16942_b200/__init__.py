@@ -20,6 +20,7 @@ from .sampler import VARIANTS, BatchCorrSampler, CorrSampler
 from .scenario import SyntheticScenario, gen_scenario
 from .sparse import (DEFAULT_CACHE_CAP_BYTES, BlockStore, PaddedGrid, ProxyBlock,
                      SparseVolumeState, compute_block_indices, gather_proxy, init_state,
+                     init_state_batch,
                      memory_footprint, padded_extent, sample_iteration, sample_iteration_raft,
                      sampled_block_mmm, set_computation_mask)
 from .types import (CacheLimitError, CentroidField, CorrvolError, CostMaps,

@@ -51,6 +51,7 @@ class PartialDesc(C.Structure):
         ("th", _i32 * MAX_LEVELS), ("tw", _i32 * MAX_LEVELS),
         ("cap_h", _i32 * MAX_LEVELS), ("cap_w", _i32 * MAX_LEVELS),
         ("tile_begin", _i32), ("tile_end", _i32),
+        ("batch", _i32),
     ]
 
 
@@ -124,7 +125,7 @@ def load(path: os.PathLike | None = None) -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.cvb_abi_version() != 1:
+    if lib.cvb_abi_version() != 2:
         raise NativeLibraryError("ABI version mismatch")
     if path is None:
         _LIB = lib

@@ -58,6 +58,8 @@ static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 b
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+// image pairs described by a partial-sampler descriptor (0 means 1)
+static inline int batch_of(const cvb_partial_desc* d) { return d->batch > 1 ? d->batch : 1; }
 
 // Function attributes live in the current device's context: opt each kernel
 // into its dynamic shared memory once per device (call sites keep `done`).

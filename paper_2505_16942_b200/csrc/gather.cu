@@ -219,7 +219,8 @@ __global__ void __launch_bounds__(WARPS * 32)
   constexpr int KK_ = K_ > 0 ? K_ * K_ : -1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tile = P.tile0 + (blockIdx.x >> 1);
-  const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
+  const TileRef tr = tile_ref(P, tile);
+  const int tile_y = tr.ty, tile_x = tr.tx;
   const int grp = (blockIdx.x & 1) * WARPS + warp;  // query group (2 rows x 4 columns)
   const int py0 = tile_y * TQH + group_qy(grp, 0), px0 = tile_x * TQW + group_qx(grp, 0);
   if (py0 >= P.h1) return;  // warp-uniform
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(WARPS * 32)
     const int py = py0 + (lane >> 2), px = px0 + (lane & 3);
     valid = py < P.h1 && px < P.w1;
     double x = 0.0, y = 0.0;
-    if (valid) load_coord(P.coords, P.f64, (int64_t)py * P.w1 + px, x, y);
+    if (valid) load_coord(P.coords, P.f64, tr.pix + (int64_t)py * P.w1 + px, x, y);
     for (int li = 0; li < nlev; ++li) {
       const int l = level0 + li;
       QInfo qi{0, 0, 0.0, 0.0, Weights32{0.f, 0.f, 0.f, 0.f}};
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   const unsigned vmask = __ballot_sync(0xffffffffu, valid) & 0xFFu;
   __syncwarp();
   if (vmask == 0) return;
-  const int64_t pix0 = (int64_t)py0 * P.w1 + px0;
+  const int64_t pix0 = tr.pix + (int64_t)py0 * P.w1 + px0;
   auto pix = [&](int q) { return pix0 + (q >> 2) * (int64_t)P.w1 + (q & 3); };
   float* O = sm.outs[warp];
   uint32_t phase0 = 0u, phase1 = 0u;
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(WARPS * 32)
     }
     // per query: (2r+2)^2 patch from the cache, or direct dots if overflowed
     const int d = P.d;
-    const float* f2 = P.f2[l];
+    const float* f2 = P.f2[l] + tr.pair * P.f2_pp[l];
     for (int q = 0; q < TQW; ++q) {
       if ((done >> q) & 1u) continue;
       const float* a = P.f1 + pix(q) * d;

@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
   pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tile = P.tile0 + blockIdx.x / CTAS_PER_TILE;
-  const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
+  const TileRef tr = tile_ref(P, tile);
+  const int tile_y = tr.ty, tile_x = tr.tx;
   // query group: tile rows 2(g>>1)..+1, columns 4(g&1)..+3
   const int grp = (int)(blockIdx.x % CTAS_PER_TILE) * WARPS + warp;
   const int py0 = tile_y * TQH + group_qy(grp, 0), px0 = tile_x * TQW + group_qx(grp, 0);
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
     status = P.meta[(tile * P.levels + l) * CVB_META_INTS + 4];
     if (qvalid) {
       double x, y;
-      load_coord(P.coords, P.f64, (int64_t)py * P.w1 + px, x, y);
+      load_coord(P.coords, P.f64, tr.pix + (int64_t)py * P.w1 + px, x, y);
       const LevelPos lp = level_pos(x, y, l);
       ay = clamp_anchor(lp.y0, R, P.th[l]);
       ax = clamp_anchor(lp.x0, R, P.tw[l]);
@@ -138,12 +139,14 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
     }
   }
   if (vmask == 0) return;
-  const int64_t pix0 = (int64_t)py0 * P.w1 + px0;  // pixel of query i: pix0 + (i>>2)*W + (i&3)
+  // pixel of query i (within the pair's frame): pix0 + (i>>2)*W + (i&3)
+  const int64_t pix0 = (int64_t)py0 * P.w1 + px0;
   float* O = sm.outs[warp];  // [q][nlev][81]
   // overflowed levels: warp-cooperative direct dots (warp-uniform loop)
   for (int l_ = 0; l_ < nlev; ++l_) {
     if (__shfl_sync(0xffffffffu, status, 8 * l_) == ST_OVERFLOW)
-      overflow_level(P.f1, P.f2[level0 + l_], P.th[level0 + l_], P.tw[level0 + l_], P.d, P.vec,
+      overflow_level(P.f1 + tr.pix * P.d, P.f2[level0 + l_] + tr.pair * P.f2_pp[level0 + l_],
+                     P.th[level0 + l_], P.tw[level0 + l_], P.d, P.vec,
                      pix0, P.w1, vmask, ay, ax, w, l_, nlev, sm.patch[warp], O, lane);
   }
   // every lane (q, l) combines the 81 taps of query q at level l, three tap
@@ -201,12 +204,13 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
     // RAFT CorrBlock layout: out[(l * 81 + dx * 9 + dy) * H * W + pixel]; per
     // window index each row of the group is 16 contiguous bytes
     const int64_t hw = (int64_t)P.h1 * P.w1;
+    float* out_pair = out + tr.pair * (int64_t)P.levels * KK * hw;  // [B, L*81, H, W]
     for (int e = lane; e < nlev * KK * 2; e += 32) {
       const int hq = e & 1, lt = e >> 1;
       const int l_ = lt / KK, t = lt - l_ * KK;
       const int dy = t / K, dx = t - dy * K;
       const unsigned rowmask = (vmask >> (4 * hq)) & 0xFu;
-      float* dst = out + ((int64_t)(level0 + l_) * KK + dx * K + dy) * hw + pix0 + hq * P.w1;
+      float* dst = out_pair + ((int64_t)(level0 + l_) * KK + dx * K + dy) * hw + pix0 + hq * P.w1;
       const float* src = O + (4 * hq) * nlev * KK + lt;
       if (rowmask == 0xFu && (((uintptr_t)dst) & 15) == 0) {
         *reinterpret_cast<float4*>(dst) =
@@ -220,7 +224,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
     for (int hq = 0; hq < 2; ++hq) {
       const unsigned rowmask = (vmask >> (4 * hq)) & 0xFu;
       const float* src = O + 4 * hq * nlev * KK;
-      float* dst = out + (pix0 + hq * P.w1) * (int64_t)(P.levels * KK);
+      float* dst = out + (tr.pix + pix0 + hq * P.w1) * (int64_t)(P.levels * KK);
       if (rowmask == 0xFu && nlev == P.levels && (((uintptr_t)dst) & 15) == 0) {
         // 4 consecutive pixels x L x 81 floats: one contiguous block
         const int n4 = 4 * nlev * KK / 4;

@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(GEMM_THREADS) partial_contract_kernel(PartialP
 
   const int64_t tile = P.tile0 + blockIdx.x;
   const int level = blockIdx.y;
-  const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
+  const TileRef tr = tile_ref(P, tile);
+  const int tile_y = tr.ty, tile_x = tr.tx;
   const int tw = P.tw[level];
   const int tid = threadIdx.x;
   plan_tile_level(P, tile, level, &s_plan, s_red);
@@ -45,7 +46,7 @@ __global__ void __launch_bounds__(GEMM_THREADS) partial_contract_kernel(PartialP
   const Box B = s_plan.B, I = s_plan.I;
   const bool has_i = s_plan.has_i;
   const int ch = P.ch[level], cw = P.cw[level];
-  const float* f2 = P.f2[level];
+  const float* f2 = P.f2[level] + tr.pair * P.f2_pp[level];
   float* cache = P.cache[level] + tile * (int64_t)(ch * cw) * TQ;
   const int d = P.d;
 
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(GEMM_THREADS) partial_contract_kernel(PartialP
   for (int s = 0; s < 2; ++s) {
     const int q = (tid >> 3) + 32 * s;
     const int py = tile_y * TQH + q / TQW, px = tile_x * TQW + q % TQW;
-    rowsA[s] = (py < P.h1 && px < P.w1) ? P.f1 + ((int64_t)py * P.w1 + px) * d : nullptr;
+    rowsA[s] = (py < P.h1 && px < P.w1) ? P.f1 + (tr.pix + (int64_t)py * P.w1 + px) * d : nullptr;
   }
   const int tx = tid & 15, ty = tid >> 4;
   for (int c0 = 0; c0 < n_new; c0 += GT) {
@@ -99,7 +100,8 @@ int cvb_partial_sizes(const cvb_partial_desc* desc, int64_t* n_tiles, int64_t* m
                       int64_t* cache_floats_per_level) {
   CVB_REQUIRE(desc, "partial_sizes: null desc");
   CVB_REQUIRE(desc->levels >= 1 && desc->levels <= CVB_MAX_LEVELS, "bad level count");
-  const int64_t nt = ceil_div(desc->h1, TQH) * ceil_div(desc->w1, TQW);
+  CVB_REQUIRE(desc->batch >= 0, "bad batch");
+  const int64_t nt = ceil_div(desc->h1, TQH) * ceil_div(desc->w1, TQW) * batch_of(desc);
   if (n_tiles) *n_tiles = nt;
   // per-level metadata, then one plan record per tile (tensor-core path)
   // (plus one record's worth of ints for the contraction's tile counter)
@@ -171,9 +173,13 @@ __attribute__((visibility("hidden"))) int cvb_internal_build_params(
   P.coords = coords;
   P.meta = meta;
   P.counters = counters;
-  P.plans = meta + ceil_div(desc->h1, TQH) * ceil_div(desc->w1, TQW) * desc->levels * CVB_META_INTS;
   P.tiles_x = (int)ceil_div(desc->w1, TQW);
-  P.n_tiles = ceil_div(desc->h1, TQH) * (int64_t)P.tiles_x;
+  P.batch = batch_of(desc);
+  P.tiles_pp = ceil_div(desc->h1, TQH) * (int64_t)P.tiles_x;
+  P.n_tiles = P.tiles_pp * P.batch;
+  P.plans = meta + P.n_tiles * desc->levels * CVB_META_INTS;
+  for (int l = 0; l < CVB_MAX_LEVELS; ++l)
+    P.f2_pp[l] = l < desc->levels ? (int64_t)desc->th[l] * desc->tw[l] * desc->d : 0;
   P.scale = scale;
   P.f64 = flags & CVB_COORDS_F64;
   P.normalize = scale != 1.0f;

@@ -31,12 +31,32 @@ struct PartialParams {
   int32_t* plans;        // PlanRec per tile (after the per-level meta, same buffer)
   unsigned long long* counters;
   int tiles_x;
-  int64_t n_tiles;       // all tiles of the frame
+  int64_t n_tiles;       // all tiles of the frame (of every pair of the batch)
+  int batch;             // image pairs sharing one launch (>= 1)
+  int64_t tiles_pp;      // tiles per pair: pair b owns tiles [b*tiles_pp, (b+1)*tiles_pp)
+  int64_t f2_pp[CVB_MAX_LEVELS];  // floats between consecutive pairs' level-l maps
   int64_t tile0, ntile;  // range handled by this launch
   float scale;
   bool f64, normalize, no_cache, vec;
   bool out_raft;         // CVB_OUT_RAFT output layout
 };
+
+// Where a (global) tile lives: its pair, its tile row / column within the
+// pair's frame, and the pair's first pixel in f1 / coords / the cost map
+// ([B, H, W, ...] layouts).  A batch of one reduces to the single-pair frame.
+struct TileRef {
+  int pair, ty, tx;
+  int64_t pix;
+};
+__device__ __forceinline__ TileRef tile_ref(const PartialParams& P, int64_t tile) {
+  TileRef t;
+  t.pair = P.batch > 1 ? (int)(tile / P.tiles_pp) : 0;
+  const int64_t lt = tile - (int64_t)t.pair * P.tiles_pp;
+  t.ty = (int)(lt / P.tiles_x);
+  t.tx = (int)(lt - (int64_t)t.ty * P.tiles_x);
+  t.pix = (int64_t)t.pair * P.h1 * P.w1;
+  return t;
+}
 
 struct Box {
   int ylo, yhi, xlo, xhi;
@@ -112,7 +132,8 @@ constexpr int PLAN_INTS = (int)(sizeof(PlanRec) / 4);
 // writes the new meta and counters.  `plan` and `red` are shared memory.
 __device__ __forceinline__ void plan_tile_level(const PartialParams& P, int64_t tile, int level,
                                                 TilePlan* plan, int* red) {
-  const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
+  const TileRef tr = tile_ref(P, tile);
+  const int tile_y = tr.ty, tile_x = tr.tx;
   const int th = P.th[level], tw = P.tw[level], r = P.radius;
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -127,7 +148,7 @@ __device__ __forceinline__ void plan_tile_level(const PartialParams& P, int64_t 
     const int py = tile_y * TQH + tid / TQW, px = tile_x * TQW + tid % TQW;
     if (py < P.h1 && px < P.w1) {
       double x, y;
-      load_coord(P.coords, P.f64, (int64_t)py * P.w1 + px, x, y);
+      load_coord(P.coords, P.f64, tr.pix + (int64_t)py * P.w1 + px, x, y);
       const LevelPos lp = level_pos(x, y, level);
       const int ay = clamp_anchor(lp.y0, r, th), ax = clamp_anchor(lp.x0, r, tw);
       atomicMin(&red[0], ay);
@@ -174,95 +195,6 @@ __device__ __forceinline__ void plan_tile_level(const PartialParams& P, int64_t 
     if (P.counters != nullptr) {
       if (n_new > 0) {
         atomicAdd(P.counters + 0, (unsigned long long)n_new * nvalid);
-        atomicAdd(P.counters + 1, (unsigned long long)n_new);
-      }
-      if (status == ST_OVERFLOW) atomicAdd(P.counters + 2, 1ULL);
-      if (status == ST_EMPTY) atomicAdd(P.counters + 3, 1ULL);
-    }
-  }
-  __syncthreads();
-}
-
-// Window-union tiler for ALL levels of one tile in a single pass over the
-// tile's centroids (one coordinate load per query): threads 0..63 reduce
-// their per-level anchors with warp shuffles, the two partial results per
-// level meet in shared memory, and thread l finalises level l exactly like
-// plan_tile_level.  blockDim >= 64 and >= levels.
-__device__ __forceinline__ void plan_tile_all_levels(const PartialParams& P, int64_t tile,
-                                                     TilePlan* plans, int (*red)[2][4],
-                                                     int* nvalid) {
-  const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int r = P.radius;
-  if (tid < TQ) {
-    const int py = tile_y * TQH + tid / TQW, px = tile_x * TQW + tid % TQW;
-    const bool valid = py < P.h1 && px < P.w1;
-    double x = 0.0, y = 0.0;
-    if (valid) load_coord(P.coords, P.f64, (int64_t)py * P.w1 + px, x, y);
-    const unsigned vote = __ballot_sync(0xffffffffu, valid);
-    if (lane == 0) atomicAdd(nvalid, __popc(vote));
-    for (int l = 0; l < P.levels; ++l) {
-      int ylo = INT_MAX, yhi = INT_MIN, xlo = INT_MAX, xhi = INT_MIN;
-      if (valid) {
-        const LevelPos lp = level_pos(x, y, l);
-        ylo = yhi = clamp_anchor(lp.y0, r, P.th[l]);
-        xlo = xhi = clamp_anchor(lp.x0, r, P.tw[l]);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        ylo = min(ylo, __shfl_xor_sync(0xffffffffu, ylo, o));
-        yhi = max(yhi, __shfl_xor_sync(0xffffffffu, yhi, o));
-        xlo = min(xlo, __shfl_xor_sync(0xffffffffu, xlo, o));
-        xhi = max(xhi, __shfl_xor_sync(0xffffffffu, xhi, o));
-      }
-      if (lane == 0) {
-        red[l][w][0] = ylo;
-        red[l][w][1] = yhi;
-        red[l][w][2] = xlo;
-        red[l][w][3] = xhi;
-      }
-    }
-  }
-  __syncthreads();
-  if (tid < P.levels) {
-    const int level = tid;
-    const int th = P.th[level], tw = P.tw[level];
-    int32_t* meta = P.meta + (tile * P.levels + level) * CVB_META_INTS;
-    const int nv = *nvalid;
-    Box B;
-    B.ylo = max(min(red[level][0][0], red[level][1][0]) - r, 0);
-    B.yhi = min(max(red[level][0][1], red[level][1][1]) + r + 1, th - 1);
-    B.xlo = max(min(red[level][0][2], red[level][1][2]) - r, 0);
-    B.xhi = min(max(red[level][0][3], red[level][1][3]) + r + 1, tw - 1);
-    int status = ST_OK;
-    if (nv == 0 || B.empty()) {
-      status = ST_EMPTY;
-      B = Box{1, 0, 1, 0};
-    } else if (B.h() > P.ch[level] || B.w() > P.cw[level]) {
-      status = ST_OVERFLOW;
-    }
-    const Box prev{meta[0], meta[1], meta[2], meta[3]};
-    const bool prev_ok = !P.no_cache && meta[4] == ST_OK && !prev.empty();
-    const Box I{max(B.ylo, prev.ylo), min(B.yhi, prev.yhi), max(B.xlo, prev.xlo),
-                min(B.xhi, prev.xhi)};
-    const bool has_i = status == ST_OK && prev_ok && !I.empty();
-    const int n_new = status == ST_OK ? (int)(B.area() - (has_i ? I.area() : 0)) : 0;
-    TilePlan& plan = plans[level];
-    plan.B = B;
-    plan.I = I;
-    plan.has_i = has_i;
-    plan.n_new = n_new;
-    plan.nvalid = nv;
-    plan.status = status;
-    meta[0] = B.ylo;
-    meta[1] = B.yhi;
-    meta[2] = B.xlo;
-    meta[3] = B.xhi;
-    meta[4] = status;
-    meta[5] = n_new;
-    if (P.counters != nullptr) {
-      if (n_new > 0) {
-        atomicAdd(P.counters + 0, (unsigned long long)n_new * nv);
         atomicAdd(P.counters + 1, (unsigned long long)n_new);
       }
       if (status == ST_OVERFLOW) atomicAdd(P.counters + 2, 1ULL);

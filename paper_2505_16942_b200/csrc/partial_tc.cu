@@ -214,6 +214,7 @@ struct TcParams {
   const __half* f2s[CVB_MAX_LEVELS];   // hi plane [th*tw][dp]; lo = hi + plane
   const int8_t* e2[CVB_MAX_LEVELS];    // per cell exponent
   int64_t plane[CVB_MAX_LEVELS];
+  int64_t pair_bytes[CVB_MAX_LEVELS];  // split-operand bytes per pair of the batch, per level
   int dp;
   int dbg;                             // profiling knockouts (CVB_TC_DEBUG; debug instantiation only)
   unsigned long long* ts;              // role timeline (CVB_TC_DEBUG & 16; debug instantiation only)
@@ -714,6 +715,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (S.tile < 0) break;
       const int n = S.n_cells;
       const int n_chunks = (n + tc::M - 1) / tc::M;
+      const int64_t pair = P.batch > 1 ? S.tile / P.tiles_pp : 0;
       for (int c = 0; c < n_chunks; ++c) {
         // source row of A row 32aw + lane (hi plane; lo = hi + plane)
         const int gi = c * tc::M + A_ROWS * aw + (lane % A_ROWS);
@@ -721,7 +723,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         int64_t my_plane = 0;
         if (gi < n) {
           const tc::CellRef cr = tc::cell_of(gi, S.plan, S.prefix, P.levels);
-          my_hi = T.f2s[cr.level] + ((int64_t)cr.cy * P.tw[cr.level] + cr.cx) * dp;
+          my_hi = reinterpret_cast<const __half*>(reinterpret_cast<const uint8_t*>(T.f2s[cr.level]) +
+                                                  pair * T.pair_bytes[cr.level]) +
+                  ((int64_t)cr.cy * P.tw[cr.level] + cr.cx) * dp;
           my_plane = T.plane[cr.level];
         }
         for (int kb = 0; kb < n_kb; ++kb, ++g) {
@@ -769,6 +773,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int64_t tile = S.tile;
       const int n = S.n_cells;
       const int n_chunks = (n + tc::M - 1) / tc::M;
+      const int64_t pair = P.batch > 1 ? tile / P.tiles_pp : 0;
       if (n_chunks > 0) {
         // the tile's 64 query scales 2^-e_q
         tc::named_bar(1, 128);
@@ -789,7 +794,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           plane = (int64_t)ch * cw * TQW;
           dst = P.cache[cr.level] + tile * plane * TQH +
                 (int64_t)slot_of(cr.cy, cr.cx, ch, cw) * TQW;
-          e_c = T.e2[cr.level][(int64_t)cr.cy * P.tw[cr.level] + cr.cx];
+          e_c = T.e2[cr.level][pair * T.pair_bytes[cr.level] + (int64_t)cr.cy * P.tw[cr.level] + cr.cx];
         }
         if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.acc_full[ab]), cg >> 1))) goto done;
         tc::tc_fence_after();
@@ -859,7 +864,8 @@ __global__ void __launch_bounds__(PLAN_WARPS * 32) plan_kernel(PartialParams P) 
   if (t < P.ntile) {
     const int64_t tile = P.tile0 + t;
     const int r = P.radius;
-    const int tile_y = (int)(tile / P.tiles_x), tile_x = (int)(tile % P.tiles_x);
+    const TileRef tr = tile_ref(P, tile);
+    const int tile_y = tr.ty, tile_x = tr.tx;
     double x[2], y[2];
     bool v[2];
 #pragma unroll
@@ -868,7 +874,7 @@ __global__ void __launch_bounds__(PLAN_WARPS * 32) plan_kernel(PartialParams P) 
       const int py = tile_y * TQH + q / TQW, px = tile_x * TQW + q % TQW;
       v[h] = py < P.h1 && px < P.w1;
       x[h] = y[h] = 0.0;
-      if (v[h]) load_coord(P.coords, P.f64, (int64_t)py * P.w1 + px, x[h], y[h]);
+      if (v[h]) load_coord(P.coords, P.f64, tr.pix + (int64_t)py * P.w1 + px, x[h], y[h]);
     }
     const int nv = __popc(__ballot_sync(0xffffffffu, v[0])) + __popc(__ballot_sync(0xffffffffu, v[1]));
     int mylo_y = 0, myhi_y = 0, mylo_x = 0, myhi_x = 0;  // lane l keeps level l
@@ -1032,21 +1038,25 @@ using namespace cvb;
 
 extern "C" {
 
+// split-operand bytes of one pair at level l: hi plane, lo plane, exponents
+static int64_t tc_pair_bytes(const cvb_partial_desc* desc, int l, int dp) {
+  const int64_t cells = (int64_t)desc->th[l] * desc->tw[l];
+  return 4 * cells * dp + ceil_div(cells, 16) * 16;
+}
+
 int cvb_tc_sizes(const cvb_partial_desc* desc, int64_t* f1_split_bytes,
                  int64_t* f2_split_bytes_per_level) {
   CVB_REQUIRE(desc, "tc_sizes: null desc");
   CVB_REQUIRE(desc->levels >= 1 && desc->levels <= CVB_MAX_LEVELS, "bad level count");
   const int dp = (int)ceil_div(desc->d, tc::KP) * tc::KP;
   CVB_REQUIRE(dp <= tc::MAX_DP, "tensor-core path supports D <= %d", tc::MAX_DP);
-  const int64_t nt = ceil_div(desc->h1, TQH) * ceil_div(desc->w1, TQW);
-  // F1: per-tile B images, then one exponent byte per query
+  const int64_t nt = ceil_div(desc->h1, TQH) * ceil_div(desc->w1, TQW) * batch_of(desc);
+  // F1: per-tile B images (tiles of every pair), then one exponent byte per query
   if (f1_split_bytes) *f1_split_bytes = nt * tc::N * dp * 4 + nt * tc::N;
-  // per level: hi plane, lo plane, then one exponent byte per cell
+  // per level and pair: hi plane, lo plane, then one exponent byte per cell
   if (f2_split_bytes_per_level)
-    for (int l = 0; l < desc->levels; ++l) {
-      const int64_t cells = (int64_t)desc->th[l] * desc->tw[l];
-      f2_split_bytes_per_level[l] = 4 * cells * dp + ceil_div(cells, 16) * 16;
-    }
+    for (int l = 0; l < desc->levels; ++l)
+      f2_split_bytes_per_level[l] = tc_pair_bytes(desc, l, dp) * batch_of(desc);
   return CVB_OK;
 }
 
@@ -1065,47 +1075,59 @@ int cvb_tc_prepare(const cvb_partial_desc* desc, const float* f1, float* const* 
   const int d = desc->d;
   const int dp = (int)ceil_div(d, tc::KP) * tc::KP;
   const int tiles_x = (int)ceil_div(desc->w1, TQW);
-  const int64_t n_tiles = ceil_div(desc->h1, TQH) * tiles_x;
-  bool vec = d % 4 == 0 && ((uintptr_t)f1 & 15) == 0;
-  uint8_t* f1s = reinterpret_cast<uint8_t*>(f1_split);
-  tc::split_f1_kernel<<<prep_grid(n_tiles * (tc::N / 8)), 256, 0, s>>>(
-      f1, desc->h1, desc->w1, d, dp, tiles_x, n_tiles, vec, f1s,
-      reinterpret_cast<int8_t*>(f1s + n_tiles * tc::N * dp * 4));
-  if ((st = check_launch("tc_split_f1")) != CVB_OK) return st;
+  const int64_t tiles_pp = ceil_div(desc->h1, TQH) * tiles_x;
+  const int batch = batch_of(desc);
+  const int64_t n_all = tiles_pp * batch;
+  const int64_t tile_bytes = (int64_t)tc::N * dp * 4;
   const bool pool = flags & CVB_PREP_POOL;
   for (int l = 0; l < desc->levels; ++l)
     CVB_REQUIRE(f2_levels_host[l] && f2_split_host[l], "tc_prepare: null level pointer");
-  auto planes_of = [&](int l) { return reinterpret_cast<__half*>(f2_split_host[l]); };
-  auto exps_of = [&](int l) {
-    return reinterpret_cast<int8_t*>(planes_of(l) + 2 * (int64_t)desc->th[l] * desc->tw[l] * dp);
-  };
   auto aligned = [&](const void* p) { return d % 4 == 0 && ((uintptr_t)p & 15) == 0; };
   // level 0 is split by the level-1 pooling pass when there is one
   const bool fuse01 = pool && desc->levels > 1;
-  for (int l = 0; l < desc->levels; ++l) {
-    const int h = desc->th[l], w = desc->tw[l];
-    const int64_t cells = (int64_t)h * w;
-    if (l == 0 && fuse01) {
-      const int64_t tail = cells - (int64_t)(h / 2) * 2 * ((w / 2) * 2);
-      if (tail > 0) {
-        tc::split_tail_kernel<<<prep_grid(tail), 256, 0, s>>>(
-            f2_levels_host[0], h, w, d, dp, aligned(f2_levels_host[0]), planes_of(0), exps_of(0));
-        if ((st = check_launch("tc_split_tail")) != CVB_OK) return st;
+  for (int b = 0; b < batch; ++b) {  // pair-major buffers: one pass per pair
+    const float* f1b_ = f1 + (int64_t)b * desc->h1 * desc->w1 * d;
+    uint8_t* f1s = reinterpret_cast<uint8_t*>(f1_split);
+    tc::split_f1_kernel<<<prep_grid(tiles_pp * (tc::N / 8)), 256, 0, s>>>(
+        f1b_, desc->h1, desc->w1, d, dp, tiles_x, tiles_pp, aligned(f1b_),
+        f1s + b * tiles_pp * tile_bytes,
+        reinterpret_cast<int8_t*>(f1s + n_all * tile_bytes + b * tiles_pp * tc::N));
+    if ((st = check_launch("tc_split_f1")) != CVB_OK) return st;
+    auto level_of = [&](int l) {
+      return f2_levels_host[l] + (int64_t)b * desc->th[l] * desc->tw[l] * d;
+    };
+    auto planes_of = [&](int l) {
+      return reinterpret_cast<__half*>(reinterpret_cast<uint8_t*>(f2_split_host[l]) +
+                                       b * tc_pair_bytes(desc, l, dp));
+    };
+    auto exps_of = [&](int l) {
+      return reinterpret_cast<int8_t*>(planes_of(l) + 2 * (int64_t)desc->th[l] * desc->tw[l] * dp);
+    };
+    for (int l = 0; l < desc->levels; ++l) {
+      const int h = desc->th[l], w = desc->tw[l];
+      const int64_t cells = (int64_t)h * w;
+      if (l == 0 && fuse01) {
+        const int64_t tail = cells - (int64_t)(h / 2) * 2 * ((w / 2) * 2);
+        if (tail > 0) {
+          tc::split_tail_kernel<<<prep_grid(tail), 256, 0, s>>>(
+              level_of(0), h, w, d, dp, aligned(level_of(0)), planes_of(0), exps_of(0));
+          if ((st = check_launch("tc_split_tail")) != CVB_OK) return st;
+        }
+        continue;
       }
-      continue;
+      const bool pool_l = pool && l > 0;
+      if (pool_l)
+        CVB_REQUIRE(desc->th[l - 1] / 2 == h && desc->tw[l - 1] / 2 == w,
+                    "tc_prepare: level %d dims are not the 2x2 pool of level %d", l, l - 1);
+      const float* src = pool_l ? level_of(l - 1) : level_of(l);
+      const bool v = aligned(src) && aligned(level_of(l));
+      const bool split_src = fuse01 && l == 1;
+      tc::split_level_kernel<<<prep_grid(cells), 256, 0, s>>>(
+          src, pool_l ? desc->tw[l - 1] : w, level_of(l), h, w, d, dp, pool_l, v, planes_of(l),
+          exps_of(l), split_src ? planes_of(0) : nullptr, split_src ? exps_of(0) : nullptr,
+          (int64_t)desc->th[0] * desc->tw[0]);
+      if ((st = check_launch("tc_split_level")) != CVB_OK) return st;
     }
-    const bool pool_l = pool && l > 0;
-    if (pool_l)
-      CVB_REQUIRE(desc->th[l - 1] / 2 == h && desc->tw[l - 1] / 2 == w,
-                  "tc_prepare: level %d dims are not the 2x2 pool of level %d", l, l - 1);
-    const float* src = pool_l ? f2_levels_host[l - 1] : f2_levels_host[l];
-    const bool v = aligned(src) && aligned(f2_levels_host[l]);
-    const bool split_src = fuse01 && l == 1;
-    tc::split_level_kernel<<<prep_grid(cells), 256, 0, s>>>(
-        src, pool_l ? desc->tw[l - 1] : w, f2_levels_host[l], h, w, d, dp, pool_l, v, planes_of(l),
-        exps_of(l), split_src ? planes_of(0) : nullptr, split_src ? exps_of(0) : nullptr,
-        (int64_t)desc->th[0] * desc->tw[0]);
-    if ((st = check_launch("tc_split_level")) != CVB_OK) return st;
   }
   return CVB_OK;
 }
@@ -1130,6 +1152,7 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
     const bool used = l < desc->levels;
     T.f2s[l] = used ? reinterpret_cast<const __half*>(f2_split_host[l]) : nullptr;
     T.plane[l] = used ? (int64_t)desc->th[l] * desc->tw[l] * T.dp : 0;
+    T.pair_bytes[l] = used ? tc_pair_bytes(desc, l, T.dp) : 0;
     T.e2[l] = used ? reinterpret_cast<const int8_t*>(T.f2s[l] + 2 * T.plane[l]) : nullptr;
     if (used) CVB_REQUIRE(T.f2s[l], "partial_contract_tc: null level pointer");
   }

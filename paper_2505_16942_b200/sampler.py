@@ -22,7 +22,7 @@ import torch
 
 from .dense import build_feature_pyramid, build_volume_pyramid, estimate_dense_bytes, lookup_dense
 from .ondemand import lookup_on_demand
-from .sparse import init_state, memory_footprint, sample_iteration
+from .sparse import init_state, init_state_batch, memory_footprint, sample_iteration
 from .types import CentroidField, CostMaps, FeatureMap, LookupSpec
 
 VARIANTS = ("dense", "ondemand", "partial")
@@ -135,38 +135,96 @@ class BatchCorrSampler:
     """A batch of independent image pairs (C5: batched 4K sweep).
 
     fmaps1 / fmaps2: [B, H, W, D]; `__call__(coords [B, H, W, 2])` returns
-    [B, H, W, L, 2r+1, 2r+1].  Each pair keeps its own state (the reference
-    has no batching), so pairs shard across ranks with no
-    data-path collective (`parallel.batch_slices`); `parallel.gather_bands`
-    all-gathers the per-rank slices when a caller needs every pair's costs
-    on every rank.
+    [B, H, W, L, 2r+1, 2r+1].  The partial variant keeps ONE tile-mode state
+    for all pairs (`sparse.init_state_batch`): each iteration is one plan,
+    one contraction and one sampler launch over every pair's tiles, and with
+    graph=True (default) the iteration is replayed from a captured CUDA graph.
+    Per pair the costs are bit-identical to a single-pair CorrSampler.  Pairs
+    shard across ranks with no data-path collective (`parallel.batch_slices`);
+    `parallel.gather_bands` all-gathers the per-rank slices when every rank
+    needs every pair's costs.  The reference has no batching.
+    The dense / on-demand variants run pair by pair.
     """
 
     def __init__(self, fmaps1: torch.Tensor, fmaps2: torch.Tensor, spec: LookupSpec,
-                 variant: str = "partial", **kwargs):
+                 variant: str = "partial", strict: bool = False, cache: bool = True,
+                 graph: bool = True, **kwargs):
         if fmaps1.dim() != 4 or fmaps1.shape != fmaps2.shape:
             raise ValueError("fmaps must both be [B, H, W, D] with equal shapes")
+        variant = _ALIASES.get(variant, variant)
         self.spec = spec
-        self.samplers = [CorrSampler(FeatureMap(fmaps1[b], check=False),
-                                     FeatureMap(fmaps2[b], check=False), spec, variant=variant,
-                                     check=False, **kwargs)
-                         for b in range(fmaps1.shape[0])]
+        self.variant = variant
+        self.batch, self.height, self.width = fmaps1.shape[:3]
+        self.state = None
+        self.samplers = []
+        self.graph = graph and variant == "partial"
+        self._graph = None
+        self._g_coords = None
+        self._g_out = None
+        self._own_out = None
+        self._calls = 0
+        if variant == "partial":
+            self.state = init_state_batch(fmaps1, fmaps2, spec, strict=strict,
+                                          cache_enabled=cache, **kwargs)
+        else:
+            self.samplers = [CorrSampler(FeatureMap(fmaps1[b], check=False),
+                                         FeatureMap(fmaps2[b], check=False), spec,
+                                         variant=variant, strict=strict, cache=cache,
+                                         check=False, **kwargs)
+                             for b in range(fmaps1.shape[0])]
 
     def __len__(self) -> int:
-        return len(self.samplers)
+        return self.batch
 
     def states(self):
-        """Per-pair partial-sampler states (device counters, footprints)."""
-        return [s.state for s in self.samplers]
+        """The partial-sampler state(s): one batched state (device counters,
+        footprint)."""
+        return [self.state] if self.state is not None else [s.state for s in self.samplers]
+
+    def _out_shape(self):
+        k = self.spec.window
+        return (self.batch, self.height, self.width, self.spec.levels, k, k)
 
     def __call__(self, coords: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         b, h, w = coords.shape[:3]
-        if b != len(self.samplers):
-            raise ValueError(f"coords batch {b} != {len(self.samplers)} pairs")
-        k = self.spec.window
+        if (b, h, w) != (self.batch, self.height, self.width):
+            raise ValueError(f"coords {tuple(coords.shape)} do not match the batch "
+                             f"[{self.batch}, {self.height}, {self.width}, 2]")
         if out is None:
-            out = torch.empty((b, h, w, self.spec.levels, k, k), dtype=torch.float32,
-                              device=coords.device)
-        for i, s in enumerate(self.samplers):
-            s(CentroidField(coords[i], check=False), out=out[i])
+            if self.graph and self.state is not None:
+                # graph mode: one persistent result buffer, reused by the next call
+                if self._own_out is None:
+                    self._own_out = torch.empty(self._out_shape(), dtype=torch.float32,
+                                                device=coords.device)
+                out = self._own_out
+            else:
+                out = torch.empty(self._out_shape(), dtype=torch.float32, device=coords.device)
+        if self.state is None:
+            for i, s in enumerate(self.samplers):
+                s(CentroidField(coords[i], check=False), out=out[i])
+            return out
+        flat = coords.reshape(b * h, w, 2)
+        view = out.view(b * h, w, *out.shape[3:])
+        if not self.graph or self._calls == 0:  # eager (the first call sets up, iteration 0)
+            self._calls += 1
+            sample_iteration(self.state, CentroidField(flat, check=False), out=view)
+            return out
+        # one captured iteration per output buffer: callers that reuse `out`
+        # (the usual loop) replay it with no extra copy of the cost maps
+        if self._graph is None or self._g_out != out.data_ptr() or \
+                flat.dtype != self._g_coords.dtype:
+            self._g_coords = torch.empty_like(flat)
+            self._g_coords.copy_(flat)
+            g_cents = CentroidField(self._g_coords, check=False)
+            torch.cuda.synchronize(flat.device)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                sample_iteration(self.state, g_cents, out=view)
+            self.state.iteration -= 1  # capture recorded the launches without running them
+            self._graph, self._g_out = graph, out.data_ptr()
+        else:
+            self._g_coords.copy_(flat)
+        self._graph.replay()
+        self.state.iteration += 1
+        self._calls += 1
         return out

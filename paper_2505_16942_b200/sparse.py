@@ -295,6 +295,7 @@ class SparseVolumeState:
         self.tc_f2 = None
         self.ref_counters = False
         self._ref_counts = None
+        self.batch = 1
 
     # -- reference-compatible attributes ------------------------------------
     @property
@@ -416,49 +417,8 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
     state = SparseVolumeState(f1, spec, block, pm1, pyr, levels, cache_enabled, backend, mode,
                               strict)
     if mode == "tile":
-        if spec.radius > 8:
-            raise ValueError("tile mode supports radius <= 8")
-        desc = _lib.PartialDesc()
-        desc.h1, desc.w1, desc.d = f1.height, f1.width, f1.dims
-        desc.levels, desc.radius = spec.levels, spec.radius
-        caps = _tile_caps(spec, tile_caps)
-        for lvl, lv in enumerate(levels):
-            desc.th[lvl], desc.tw[lvl] = lv.tgt_shape
-            desc.cap_h[lvl], desc.cap_w[lvl] = caps[lvl]
-            lv.cap = caps[lvl]
-        n_tiles = _lib.C.c_int64()
-        meta_ints = _lib.C.c_int64()
-        per_level = (_lib.C.c_int64 * _lib.MAX_LEVELS)()
-        _lib.call("cvb_partial_sizes", _lib.C.byref(desc), _lib.C.byref(n_tiles),
-                  _lib.C.byref(meta_ints), per_level)
-        total = 4 * sum(per_level[i] for i in range(spec.levels))
-        if hard_limit_bytes is not None and total > hard_limit_bytes:
-            raise CacheLimitError(
-                f"tile cache needs {total} bytes, hard limit is {hard_limit_bytes}")
-        state.desc = desc
-        state.n_tiles = n_tiles.value
-        state.meta = torch.empty(meta_ints.value, dtype=torch.int32, device=dev)
-        for lvl, lv in enumerate(levels):
-            lv.cache = torch.empty(per_level[lvl], dtype=torch.float32, device=dev)
-        _lib.call("cvb_partial_reset", _lib.C.byref(desc), _lib.ptr(state.meta),
-                  stream_handle())
-        if ref_counters:
-            state.ref_counters = True
-            state._ref_counts = torch.zeros(1 + spec.levels, dtype=torch.int64, device=dev)
-            for lvl, lv in enumerate(levels):
-                n_src, wpr = pm1.n_tiles, lv.words_per_row
-                lv.mask_cum_bits = torch.zeros((n_src, wpr), dtype=torch.int32, device=dev)
-                lv.mask_union_bits = torch.zeros((n_src, wpr), dtype=torch.int32, device=dev)
-                lv.store = _StoreCount(state._ref_counts, 1 + lvl, 4 * block ** 4)
-        if tensor_cores:
-            _prepare_tc(state, pool=fuse_pyramid)
-            # overlap contraction and gathering across tile ranges when the frame
-            # spans many waves (>= 8 tiles per SM)
-            if pipeline_splits is None:
-                # measured on B200 at C4: no gain (the contraction's shared
-                # memory keeps the sampler from co-residing), so off by default
-                pipeline_splits = 1
-            state.pipeline_splits = max(1, int(pipeline_splits))
+        _setup_tile(state, tile_caps, hard_limit_bytes, tensor_cores, fuse_pyramid,
+                    pipeline_splits, ref_counters)
     else:
         for lv in levels:
             n_src, wpr = pm1.n_tiles, lv.words_per_row
@@ -468,6 +428,108 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
             lv.store = BlockStore(block, growth_factor=growth_factor,
                                   overalloc_cap_bytes=cache_cap_bytes,
                                   hard_limit_bytes=hard_limit_bytes, device=dev)
+    return state
+
+
+def _setup_tile(state: SparseVolumeState, tile_caps, hard_limit_bytes: Optional[int],
+                tensor_cores: bool, fuse_pyramid: bool, pipeline_splits: Optional[int],
+                ref_counters: bool, batch: int = 1, pair_height: Optional[int] = None) -> None:
+    """Tile-mode device state: descriptor, metadata, tile caches (all pairs of
+    a batch), optional reference-model counters, split operands."""
+    spec, levels, dev = state.spec, state.levels, state.device
+    if spec.radius > 8:
+        raise ValueError("tile mode supports radius <= 8")
+    desc = _lib.PartialDesc()
+    desc.h1 = state.f1.height if pair_height is None else pair_height
+    desc.w1, desc.d = state.f1.width, state.f1.dims
+    desc.levels, desc.radius = spec.levels, spec.radius
+    desc.batch = batch
+    caps = _tile_caps(spec, tile_caps)
+    for lvl, lv in enumerate(levels):
+        desc.th[lvl], desc.tw[lvl] = lv.tgt_shape
+        desc.cap_h[lvl], desc.cap_w[lvl] = caps[lvl]
+        lv.cap = caps[lvl]
+    n_tiles = _lib.C.c_int64()
+    meta_ints = _lib.C.c_int64()
+    per_level = (_lib.C.c_int64 * _lib.MAX_LEVELS)()
+    _lib.call("cvb_partial_sizes", _lib.C.byref(desc), _lib.C.byref(n_tiles),
+              _lib.C.byref(meta_ints), per_level)
+    total = 4 * sum(per_level[i] for i in range(spec.levels))
+    if hard_limit_bytes is not None and total > hard_limit_bytes:
+        raise CacheLimitError(
+            f"tile cache needs {total} bytes, hard limit is {hard_limit_bytes}")
+    state.desc = desc
+    state.batch = batch
+    state.n_tiles = n_tiles.value
+    state.meta = torch.empty(meta_ints.value, dtype=torch.int32, device=dev)
+    for lvl, lv in enumerate(levels):
+        lv.cache = torch.empty(per_level[lvl], dtype=torch.float32, device=dev)
+    _lib.call("cvb_partial_reset", _lib.C.byref(desc), _lib.ptr(state.meta), stream_handle())
+    if ref_counters:
+        if batch > 1:
+            raise ValueError("ref_counters needs a single-pair state")
+        state.ref_counters = True
+        state._ref_counts = torch.zeros(1 + spec.levels, dtype=torch.int64, device=dev)
+        for lvl, lv in enumerate(levels):
+            n_src, wpr = state.pm1.n_tiles, lv.words_per_row
+            lv.mask_cum_bits = torch.zeros((n_src, wpr), dtype=torch.int32, device=dev)
+            lv.mask_union_bits = torch.zeros((n_src, wpr), dtype=torch.int32, device=dev)
+            lv.store = _StoreCount(state._ref_counts, 1 + lvl, 4 * state.block ** 4)
+    if tensor_cores:
+        _prepare_tc(state, pool=fuse_pyramid)
+        # overlap contraction and gathering across tile ranges: measured on
+        # B200 at C4, no gain (the contraction's shared memory keeps the
+        # sampler from co-residing), so off by default
+        state.pipeline_splits = max(1, int(pipeline_splits or 1))
+
+
+@on_device
+def init_state_batch(f1: torch.Tensor, f2: torch.Tensor, spec: LookupSpec, strict: bool = False,
+                     cache_enabled: bool = True, tile_caps=None,
+                     hard_limit_bytes: Optional[int] = None,
+                     tensor_cores: Optional[bool] = None) -> SparseVolumeState:
+    """One tile-mode state for B image pairs of equal geometry (C5).
+
+    f1, f2: [B, H, W, D] CUDA tensors.  Every iteration is ONE plan, ONE
+    contraction and ONE sampler launch over all pairs' tiles (the pair index
+    is folded into the tile id, csrc/partial.cuh `tile_ref`); per-pair
+    pyramids, caches, metadata and split operands live in pair-major arenas.
+    `sample_iteration(state, coords)` takes coords [B*H, W, 2] (a
+    [B, H, W, 2] tensor viewed as one tall field) and returns [B*H, W, L,
+    2r+1, 2r+1]; `BatchCorrSampler` does the reshaping.  Per pair the
+    results are bit-identical to a single-pair state (same kernels, same
+    per-query arithmetic)."""
+    if f1.dim() != 4 or f1.shape != f2.shape:
+        raise ValueError("f1 and f2 must both be [B, H, W, D] with equal shapes")
+    require_cuda(f1, f2)
+    b, h, w, d = f1.shape
+    if tensor_cores is None:
+        tensor_cores = (not strict) and d <= 256
+    if tensor_cores and strict:
+        raise ValueError("strict arithmetic runs on the FP32 pipe; tensor_cores=False")
+    f1 = f1.to(torch.float32).contiguous()
+    f2 = f2.to(torch.float32).contiguous()
+    dev = f1.device
+    fh, fw = pooled_dims((h, w), spec.levels - 1)
+    if fh < 1 or fw < 1:
+        raise ValueError(f"pyramid of {spec.levels} levels on {h}x{w} would produce an empty "
+                         "level")
+    dims = [pooled_dims((h, w), l) for l in range(spec.levels)]
+    lv_t = [f2] + [torch.empty((b, th, tw, d), dtype=torch.float32, device=dev)
+                   for th, tw in dims[1:]]
+    if not tensor_cores:  # the fused split pools on the tensor-core path
+        for i in range(b):
+            _lib.call("cvb_build_pyramid", _lib.ptr(f2[i]), h, w, d, spec.levels,
+                      _lib.ptr_array([t[i] for t in lv_t]), stream_handle())
+    pyr = FeaturePyramid([FeatureMap(t.view(b * t.shape[1], t.shape[2], d), check=False)
+                          for t in lv_t])
+    pm1 = PaddedGrid.of(h, w, d, 8)
+    levels = [_LevelState(tgt_shape=dims[l], pm2=PaddedGrid.of(dims[l][0], dims[l][1], d, 8))
+              for l in range(spec.levels)]
+    state = SparseVolumeState(FeatureMap(f1.view(b * h, w, d), check=False), spec, 8, pm1, pyr,
+                              levels, cache_enabled, None, "tile", strict)
+    _setup_tile(state, tile_caps, hard_limit_bytes, tensor_cores, tensor_cores, None, False,
+                batch=b, pair_height=h)
     return state
 
 

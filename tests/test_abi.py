@@ -38,7 +38,7 @@ def test_abi_version_and_launch_counter():
     from paper_2505_16942_b200 import _lib
 
     lib = _lib.load()
-    assert lib.cvb_abi_version() == 1
+    assert lib.cvb_abi_version() == 2
     assert _lib.launch_count() >= 0
 
 

@@ -113,3 +113,25 @@ def test_c4_fast_full_frame_vs_strict_all_iterations(cuda):
         diff = float((f - s).abs().max())
         assert diff / (1 + float(s.abs().max())) <= REF_GATE
         assert diff <= NS_GATE * n1 * n2
+
+
+@pytest.mark.parametrize("strict", [False, True])
+def test_batched_state_equals_single_pairs_bitwise(cuda, strict):
+    """init_state_batch (one plan / contraction / sampler launch over all
+    pairs' tiles, graph replay) == one single-pair sampler per pair, bit for
+    bit; odd frame height so pairs' last tile rows are partial."""
+    spec = cvb.LookupSpec(4, 4, True)
+    h, w, n, batch = 46, 62, 5, 3
+    scs = [cvb.gen_scenario(s, (h, w, 256), n, spec, coords_dtype=np.float32)
+           for s in range(batch)]
+    f1 = torch.stack([torch.from_numpy(s.f1) for s in scs]).to(cuda)
+    f2 = torch.stack([torch.from_numpy(s.f2) for s in scs]).to(cuda)
+    batched = cvb.BatchCorrSampler(f1, f2, spec, strict=strict)
+    assert len(batched.states()) == 1 and batched.states()[0].batch == batch
+    singles = [cvb.CorrSampler(f1[i], f2[i], spec, strict=strict) for i in range(batch)]
+    out = torch.empty((batch, h, w, 4, 9, 9), dtype=torch.float32, device=cuda)
+    for it in range(n):
+        c = torch.stack([torch.from_numpy(s.centroid_fields[it]) for s in scs]).to(cuda)
+        got = batched(c, out=out)
+        for i in range(batch):
+            assert torch.equal(got[i], singles[i](c[i]).values), (it, i)
