@@ -645,6 +645,15 @@ def main():
     dense_bytes = cvb.estimate_dense_bytes((h, w), (h, w), levels)
     if not args.no_compare and world == 1:
         compare["ondemand_ms_per_iter"] = round(timed(lambda: step("ondemand"), 1, 1) / n_iter, 3)
+
+        def ondemand_literal():  # the reference algorithm's per-query window dots (FFMA)
+            pyr = cvb.build_feature_pyramid(cvb.FeatureMap(f2_dev, check=False), levels)
+            f1m = cvb.FeatureMap(f1_dev, check=False)
+            for c in cents:
+                cvb.lookup_on_demand(f1m, pyr, c, spec, out=out)
+
+        compare["ondemand_per_query_ffma_ms_per_iter"] = round(
+            timed(ondemand_literal, 1, 1) / n_iter, 3)
         compare["partial_nocache_ms_per_iter"] = round(
             timed(lambda: step("partial", cache=False), 1, 1) / n_iter, 3)
         torch.cuda.empty_cache()

@@ -219,6 +219,19 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
                             float* const* cache_levels_host, unsigned long long* counters,
                             int32_t flags, void* stream);
 
+/* Dense all-pairs volume on tcgen05 (the fast dense variant: build_dense_volume
+ * / build_volume_pyramid(mode="pool_features"), dense.py:27-45,121-160):
+ * out_levels_host[l] (device, float32 [h1*w1, th[l]*tw[l]], row-major) =
+ * F1 . F2_l^T for every level of desc, from the split operands that
+ * cvb_tc_prepare writes (same accuracy as cvb_partial_contract_tc).  The
+ * persistent contraction kernel of the partial path runs with every cell of
+ * every level as each tile's work list and writes dense rows.  workspace:
+ * cvb_dense_tc_workspace(desc) bytes (tile work lists).  desc->batch <= 1. */
+int64_t cvb_dense_tc_workspace(const cvb_partial_desc* desc);
+int cvb_dense_tc(const cvb_partial_desc* desc, const void* f1_split,
+                 const void* const* f2_split_host, void* workspace, float* const* out_levels_host,
+                 void* stream);
+
 /* ---- access recorder / block occupancy (analyzer.py:31-116) ------------- */
 #define CVB_ACCESS_NO_TRIM 32 /* count the full (2r+2)^2 support even where the
                                  last row / column has zero bilinear weight */

@@ -86,6 +86,8 @@ SIGNATURES = {
                                  _i32, _p]),
     "cvb_partial_contract_tc": (C.c_int, [C.POINTER(PartialDesc), _p, C.POINTER(_p), _p,
                                           C.POINTER(_p), _p, _p, C.POINTER(_p), _p, _i32, _p]),
+    "cvb_dense_tc_workspace": (_i64, [C.POINTER(PartialDesc)]),
+    "cvb_dense_tc": (C.c_int, [C.POINTER(PartialDesc), _p, C.POINTER(_p), _p, C.POINTER(_p), _p]),
     "cvb_access_union": (C.c_int, [C.POINTER(_p), _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
                                    _p, _p]),
     "cvb_access_blocks": (C.c_int, [_p, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _p,

@@ -20,6 +20,8 @@
 //     memory and written with 128-bit stores.
 // Levels whose box overflowed the cache window are evaluated by direct dot
 // products, the warp cooperating on each query's window (gather.cu semantics).
+#include <stdlib.h>
+
 #include "partial.cuh"
 
 namespace cvb {
@@ -249,6 +251,14 @@ int launch_gather_fast_r4(const PartialParams& P, float* out, cudaStream_t s) {
   static std::atomic<uint64_t> attr{0};
   const int smem = (int)sizeof(gfast::Shared);
   ensure_max_smem(attr, gfast::gather_fast_kernel, smem);
+  static int carve = -2;  // experiment knob: CVB_GF_CARVEOUT (percent of the unified array as smem)
+  if (carve == -2) {
+    const char* e = getenv("CVB_GF_CARVEOUT");
+    carve = e ? atoi(e) : -1;
+    if (carve >= 0)
+      cudaFuncSetAttribute(gfast::gather_fast_kernel,
+                           cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+  }
   for (int l0 = 0; l0 < P.levels; l0 += gfast::MAXL) {
     const int nl = min(gfast::MAXL, P.levels - l0);
     launch_pdl(gfast::gather_fast_kernel, dim3((unsigned)(gfast::CTAS_PER_TILE * P.ntile)), dim3(gfast::WARPS * 32), smem,

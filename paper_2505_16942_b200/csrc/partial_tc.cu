@@ -30,6 +30,7 @@
 #include <stddef.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "partial.cuh"
 
@@ -219,6 +220,11 @@ struct TcParams {
   int dbg;                             // profiling knockouts (CVB_TC_DEBUG; debug instantiation only)
   unsigned long long* ts;              // role timeline (CVB_TC_DEBUG & 16; debug instantiation only)
   int* watchdog;                       // host-mapped error word (null: none); see wait_phase
+  // dense mode (cvb_dense_tc): every tile's "new cells" are all cells of every
+  // level and the epilogue writes the all-pairs rows dense[l][pixel][cell]
+  // instead of cache slots
+  float* dense[CVB_MAX_LEVELS];
+  int dense_mode;
 };
 
 // Operand preparation, once per image pair.  Every row (a query of F1, a
@@ -774,6 +780,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int n = S.n_cells;
       const int n_chunks = (n + tc::M - 1) / tc::M;
       const int64_t pair = P.batch > 1 ? tile / P.tiles_pp : 0;
+      const TileRef tr = tile_ref(P, tile);
       if (n_chunks > 0) {
         // the tile's 64 query scales 2^-e_q
         tc::named_bar(1, 128);
@@ -786,14 +793,20 @@ __global__ void __launch_bounds__(THREADS, 1)
         // resolve them (and issue the exponent load) before the accumulator wait
         const int gi = c * tc::M + ep;
         float* dst = nullptr;
+        float* dd = nullptr;  // dense mode: this cell's entry in the tile's first row
         int64_t plane = 0;
         int e_c = 0;
         if (gi < n) {
           const tc::CellRef cr = tc::cell_of(gi, S.plan, S.prefix, P.levels);
-          const int ch = P.ch[cr.level], cw = P.cw[cr.level];
-          plane = (int64_t)ch * cw * TQW;
-          dst = P.cache[cr.level] + tile * plane * TQH +
-                (int64_t)slot_of(cr.cy, cr.cx, ch, cw) * TQW;
+          if (T.dense_mode) {
+            plane = (int64_t)P.th[cr.level] * P.tw[cr.level];  // row length of the level
+            dd = T.dense[cr.level] + (int64_t)cr.cy * P.tw[cr.level] + cr.cx;
+          } else {
+            const int ch = P.ch[cr.level], cw = P.cw[cr.level];
+            plane = (int64_t)ch * cw * TQW;
+            dst = P.cache[cr.level] + tile * plane * TQH +
+                  (int64_t)slot_of(cr.cy, cr.cx, ch, cw) * TQW;
+          }
           e_c = T.e2[cr.level][pair * T.pair_bytes[cr.level] + (int64_t)cr.cy * P.tw[cr.level] + cr.cx];
         }
         if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.acc_full[ab]), cg >> 1))) goto done;
@@ -824,6 +837,17 @@ __global__ void __launch_bounds__(THREADS, 1)
               }
               const int g = (2 * h + r) * 2 + c;  // == qgroup(4h + 2r, 4c)
               tc::st_global_v8(dst + g * plane, o);
+            }
+          } else if (dd != nullptr) {
+            // dense rows: query q of the tile -> pixel (8ty + q/8, 8tx + q%8); a
+            // warp's lanes are consecutive cells, so each store is 128 B
+#pragma unroll 4
+            for (int j = 0; j < 32; ++j) {
+              const int q = h * 32 + j;
+              const int py = tr.ty * TQH + (q >> 3), px = tr.tx * TQW + (q & 7);
+              if (py < P.h1 && px < P.w1)
+                dd[((int64_t)py * P.w1 + px) * plane] =
+                    fmaf(vc[j], 1.f / (1 << tc::LOG2_LO), vm[j]) * (s_q[q] * s_c);
             }
           }
         }
@@ -973,6 +997,34 @@ __global__ void __launch_bounds__(PLAN_WARPS * 32) plan_kernel(PartialParams P) 
   __syncthreads();
   if (threadIdx.x < 4 && P.counters != nullptr && s_cnt[threadIdx.x])
     atomicAdd(P.counters + threadIdx.x, s_cnt[threadIdx.x]);
+}
+
+// Dense mode plans: every tile's work list is every cell of every level
+// (B = the level grid, no previous box); resets the range's work counter.
+__global__ void dense_plan_kernel(PartialParams P) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= P.n_tiles) return;
+  int* rec = P.plans + t * PLAN_INTS;
+  PlanRec pr;
+  int acc = 0;
+  for (int l = 0; l < CVB_MAX_LEVELS; ++l) {
+    TilePlan tp{Box{1, 0, 1, 0}, Box{1, 0, 1, 0}, 0, 0, 0, ST_EMPTY};
+    if (l < P.levels) {
+      tp.B = Box{0, P.th[l] - 1, 0, P.tw[l] - 1};
+      tp.n_new = P.th[l] * P.tw[l];
+      tp.nvalid = TQ;
+      tp.status = ST_OK;
+    }
+    pr.plan[l] = tp;
+    pr.prefix[l] = acc;
+    acc += tp.n_new;
+  }
+  pr.prefix[CVB_MAX_LEVELS] = acc;
+  pr.n_cells = acc;
+  pr.tile = (int)t;
+  pr.pad = 0;  // the work counter of the range starting at tile 0
+  const int* src = reinterpret_cast<const int*>(&pr);
+  for (int i = 0; i < PLAN_INTS; ++i) rec[i] = src[i];
 }
 
 size_t smem_bytes() {
@@ -1132,12 +1184,78 @@ int cvb_tc_prepare(const cvb_partial_desc* desc, const float* f1, float* const* 
   return CVB_OK;
 }
 
+int64_t cvb_dense_tc_workspace(const cvb_partial_desc* desc) {
+  if (desc == nullptr) return 0;
+  const int64_t nt = ceil_div(desc->h1, TQH) * ceil_div(desc->w1, TQW);
+  return (nt + 1) * PLAN_INTS * (int64_t)sizeof(int);
+}
+
+int cvb_dense_tc(const cvb_partial_desc* desc, const void* f1_split,
+                 const void* const* f2_split_host, void* workspace, float* const* out_levels_host,
+                 void* stream) {
+  CVB_REQUIRE(desc && f1_split && f2_split_host && workspace && out_levels_host,
+              "dense_tc: null argument");
+  CVB_REQUIRE(desc->levels >= 1 && desc->levels <= CVB_MAX_LEVELS, "bad level count");
+  CVB_REQUIRE(desc->batch <= 1, "dense_tc: one image pair");
+  CVB_REQUIRE(desc->h1 >= 1 && desc->w1 >= 1 && desc->d >= 1, "bad source dims");
+  tc::TcParams T;
+  memset(&T, 0, sizeof(T));
+  PartialParams& P = T.P;
+  P.h1 = desc->h1;
+  P.w1 = desc->w1;
+  P.d = desc->d;
+  P.levels = desc->levels;
+  P.radius = desc->radius;
+  P.tiles_x = (int)ceil_div(desc->w1, TQW);
+  P.batch = 1;
+  P.tiles_pp = ceil_div(desc->h1, TQH) * (int64_t)P.tiles_x;
+  P.n_tiles = P.tiles_pp;
+  P.tile0 = 0;
+  P.ntile = P.n_tiles;
+  P.plans = reinterpret_cast<int32_t*>(workspace);
+  T.dp = (int)ceil_div(desc->d, tc::KP) * tc::KP;
+  CVB_REQUIRE(T.dp <= tc::MAX_DP, "tensor-core path supports D <= %d", tc::MAX_DP);
+  T.f1s = reinterpret_cast<const uint8_t*>(f1_split);
+  T.e1 = reinterpret_cast<const int8_t*>(T.f1s + P.n_tiles * tc::N * T.dp * 4);
+  for (int l = 0; l < desc->levels; ++l) {
+    P.th[l] = desc->th[l];
+    P.tw[l] = desc->tw[l];
+    P.ch[l] = P.cw[l] = 1;
+    CVB_REQUIRE(P.th[l] >= 1 && P.tw[l] >= 1, "empty target level %d", l);
+    CVB_REQUIRE((int64_t)P.th[l] * P.tw[l] < (1LL << 28), "dense_tc: level too large");
+    CVB_REQUIRE(f2_split_host[l] && out_levels_host[l], "dense_tc: null level pointer");
+    T.f2s[l] = reinterpret_cast<const __half*>(f2_split_host[l]);
+    T.plane[l] = (int64_t)desc->th[l] * desc->tw[l] * T.dp;
+    T.pair_bytes[l] = 0;
+    T.e2[l] = reinterpret_cast<const int8_t*>(T.f2s[l] + 2 * T.plane[l]);
+    T.dense[l] = out_levels_host[l];
+  }
+  T.dense_mode = 1;
+  cudaStream_t s = as_stream(stream);
+  int* word = tcp::watchdog_word(s);
+  T.watchdog = word != nullptr ? tcp::watchdog_dev : nullptr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int n_sms = tcp::sm_count(dev);
+  const size_t smem = tcp::smem_bytes();
+  static std::atomic<uint64_t> attr{0};
+  ensure_max_smem(attr, tcp::partial_contract_tcp_kernel<false>, (int)smem);
+  tcp::dense_plan_kernel<<<(unsigned)ceil_div(P.n_tiles, 128), 128, 0, s>>>(P);
+  int st = check_launch("dense_plan");
+  if (st != CVB_OK) return st;
+  const int64_t grid = P.ntile < n_sms ? P.ntile : n_sms;
+  launch_pdl(tcp::partial_contract_tcp_kernel<false>, dim3((unsigned)grid), dim3(tcp::THREADS),
+             smem, s, T);
+  return check_launch("dense_tc");
+}
+
 int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
                             const float* const* f2_levels_host, const void* f1_split,
                             const void* const* f2_split_host, const void* coords, int32_t* meta,
                             float* const* cache_levels_host, unsigned long long* counters,
                             int32_t flags, void* stream) {
   tc::TcParams T;
+  memset(&T, 0, sizeof(T));
   int st = cvb_internal_build_params(desc, f1, f2_levels_host, coords, 1.0f, meta,
                                      cache_levels_host, counters, flags, T.P);
   if (st != CVB_OK) return st;

@@ -57,15 +57,56 @@ def build_feature_pyramid(f2: FeatureMap, levels: int) -> FeaturePyramid:
     return pyr
 
 
+def _tc_ok(f1: FeatureMap, strict: bool) -> bool:
+    return not strict and f1.dims <= 256 and f1.height * f1.width > 0
+
+
+def _dense_tc(f1: FeatureMap, maps: List[FeatureMap]) -> List[torch.Tensor]:
+    """All-pairs matrices [H1*W1, h*w] of f1 against each map, on tcgen05
+    (split-fp16, the partial path's accuracy; csrc/partial_tc.cu cvb_dense_tc)."""
+    desc = _lib.PartialDesc()
+    desc.h1, desc.w1, desc.d = f1.height, f1.width, f1.dims
+    desc.levels, desc.radius = len(maps), 0
+    for l, m in enumerate(maps):
+        if m.dims != f1.dims:
+            raise ValueError(f"feature dims differ: {f1.dims} vs {m.dims}")
+        desc.th[l], desc.tw[l] = m.height, m.width
+        desc.cap_h[l] = desc.cap_w[l] = 1
+    dev = f1.values.device
+    f1b = _lib.C.c_int64()
+    per = (_lib.C.c_int64 * _lib.MAX_LEVELS)()
+    _lib.call("cvb_tc_sizes", _lib.C.byref(desc), _lib.C.byref(f1b), per)
+    f1s = torch.empty(f1b.value, dtype=torch.uint8, device=dev)
+    f2s = [torch.empty(per[l], dtype=torch.uint8, device=dev) for l in range(len(maps))]
+    _lib.call("cvb_tc_prepare", _lib.C.byref(desc), _lib.ptr(f1.values),
+              _lib.ptr_array([m.values for m in maps]), _lib.ptr(f1s), _lib.ptr_array(f2s), 0,
+              stream_handle())
+    ws = torch.empty(int(_lib.load().cvb_dense_tc_workspace(_lib.C.byref(desc))),
+                     dtype=torch.uint8, device=dev)
+    outs = [torch.empty((f1.height * f1.width, m.height * m.width), dtype=torch.float32,
+                        device=dev) for m in maps]
+    _lib.call("cvb_dense_tc", _lib.C.byref(desc), _lib.ptr(f1s), _lib.ptr_array(f2s),
+              _lib.ptr(ws), _lib.ptr_array(outs), stream_handle())
+    return outs
+
+
 @on_device
 def build_dense_volume(f1: FeatureMap, f2: FeatureMap, backend: Optional[str] = None,
                        counter: Optional[WorkCounter] = None, strict: bool = False
                        ) -> torch.Tensor:
-    """Level-0 all-pairs matrix [H1*W1, H2*W2] float32 (dense.py:27-45)."""
+    """Level-0 all-pairs matrix [H1*W1, H2*W2] float32 (dense.py:27-45).
+
+    strict: the reference's fp32 sequential dots (SIMT, bitwise); otherwise
+    tcgen05 split-fp16 (D <= 256) within the fp32 gates."""
     resolve_backend(backend)
     if f1.dims != f2.dims:
         raise ValueError(f"feature dims differ: {f1.dims} vs {f2.dims}")
     require_cuda(f1.values, f2.values)
+    if _tc_ok(f1, strict):
+        out = _dense_tc(f1, [f2])[0]
+        if counter is not None:
+            counter.add_dots(out.shape[0] * out.shape[1], f1.dims)
+        return out
     a, b = f1.flat(), f2.flat()
     out = torch.empty((a.shape[0], b.shape[0]), dtype=torch.float32, device=a.device)
     _lib.call("cvb_corr_pairs", _lib.ptr(a), a.shape[0], _lib.ptr(b), b.shape[0], f1.dims,
@@ -139,7 +180,13 @@ def build_volume_pyramid(f1: FeatureMap, f2: FeatureMap, levels: int, mode: str 
             shapes.append(pooled_dims(shapes[-1], 1))
     else:
         pyr = build_feature_pyramid(f2, levels)
-        for lvl in range(1, levels):
+        if _tc_ok(f1, strict) and levels > 1:  # levels 1.. in one tcgen05 launch
+            mats += _dense_tc(f1, pyr.levels[1:])
+            for fmap in pyr.levels[1:]:
+                shapes.append((fmap.height, fmap.width))
+                if counter is not None:
+                    counter.add_dots(f1.height * f1.width * fmap.height * fmap.width, f1.dims)
+        for lvl in range(len(mats), levels):
             fmap = pyr.levels[lvl]
             mats.append(build_dense_volume(f1, fmap, backend=backend, counter=counter,
                                            strict=strict))

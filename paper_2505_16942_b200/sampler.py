@@ -9,9 +9,13 @@ top of the reference-named functions:
     for it in range(iters):
         costs = sampler(coords)          # [H, W, L, 2r+1, 2r+1] on the GPU
 
-variant: "partial" (sparse.py, the north-star path), "ondemand"
-(ondemand.py), "dense" (dense.py; raises MemoryError when the volume would
-not fit, the analogue of the reference bench's oom row, harness.py:330-333).
+variant: "partial" (sparse.py, the north-star path: incremental tile cache),
+"ondemand" (no state across iterations: fast arithmetic recomputes every
+query tile's window union on tcgen05 each iteration into a bounded scratch;
+strict runs the reference's per-query dots, ondemand.py), "dense" (dense.py:
+the all-pairs volume, on tcgen05 unless strict; raises MemoryError when the
+volume would not fit, the analogue of the reference bench's oom row,
+harness.py:330-333).
 """
 
 from __future__ import annotations
@@ -26,6 +30,8 @@ from .sparse import init_state, init_state_batch, memory_footprint, sample_itera
 from .types import CentroidField, CostMaps, FeatureMap, LookupSpec
 
 VARIANTS = ("dense", "ondemand", "partial")
+#: tiles per scratch range of the fast on-demand variant (8 per B200 SM)
+ONDEMAND_SCRATCH_TILES = 8 * 148
 _ALIASES = {"sparse": "partial"}
 
 
@@ -64,7 +70,16 @@ class CorrSampler:
                                     mode=mode, strict=strict, **state_kwargs)
             self.pyramid = self.state.pyramid
         elif variant == "ondemand":
-            self.pyramid = build_feature_pyramid(self.f2, spec.levels)
+            if not strict and self.f1.dims <= 256 and spec.radius <= 8:
+                # fast on-demand: every iteration recomputes each query tile's
+                # window union on tcgen05 into a bounded scratch (ranges of
+                # ONDEMAND_SCRATCH_TILES tiles) and samples it; nothing is kept
+                # across iterations (no incremental cache)
+                self.state = init_state(self.f1, self.f2, spec, block, cache_enabled=False,
+                                        mode="tile", scratch_tiles=ONDEMAND_SCRATCH_TILES)
+                self.pyramid = self.state.pyramid
+            else:  # reference arithmetic: per-query window cells, FFMA-free dots
+                self.pyramid = build_feature_pyramid(self.f2, spec.levels)
         else:
             need = estimate_dense_bytes((self.f1.height, self.f1.width),
                                         (self.f2.height, self.f2.width), spec.levels)
@@ -85,6 +100,8 @@ class CorrSampler:
                 return self._graphed(cents, out)
             return sample_iteration(self.state, cents, out=out)
         if self.variant == "ondemand":
+            if self.state is not None:
+                return sample_iteration(self.state, cents, out=out)
             return lookup_on_demand(self.f1, self.pyramid, cents, self.spec, strict=self.strict,
                                     out=out)
         return lookup_dense(self.volume, cents, self.spec, strict=self.strict, out=out)
@@ -122,7 +139,7 @@ class CorrSampler:
     def memory_bytes(self) -> int:
         """Analytic bytes the variant holds between iterations."""
         feats = self.f1.values.numel() * 4
-        if self.variant == "partial":
+        if self.state is not None:
             return memory_footprint(self.state)["total_bytes"]
         feats += sum(l.values.numel() * 4 for l in self.pyramid.levels) if self.pyramid else 0
         if self.variant == "dense":

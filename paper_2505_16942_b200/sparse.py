@@ -296,6 +296,7 @@ class SparseVolumeState:
         self.ref_counters = False
         self._ref_counts = None
         self.batch = 1
+        self.scratch_tiles = 0
 
     # -- reference-compatible attributes ------------------------------------
     @property
@@ -369,7 +370,8 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
                tile_caps=None, pyramid: Optional[FeaturePyramid] = None,
                tensor_cores: Optional[bool] = None,
                pipeline_splits: Optional[int] = None,
-               ref_counters: bool = False) -> SparseVolumeState:
+               ref_counters: bool = False,
+               scratch_tiles: Optional[int] = None) -> SparseVolumeState:
     """One-time preprocessing for an image pair (sparse.py:205-248).
 
     Builds the fmap2 pyramid on the GPU and allocates the level states.
@@ -384,6 +386,10 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
     mask_union, block_positions) that the reference harness reads
     (harness.py:244-245,406-436) — at one mask kernel + one accumulate kernel
     per level and iteration; off by default so the timed path is not taxed.
+    scratch_tiles (tile mode, cache off): keep cache windows for only this many
+    tiles and run each iteration as contract+gather over consecutive ranges
+    of that many tiles — the stateless recompute ("on-demand") configuration
+    with bounded memory.
     """
     resolve_backend(backend)
     if f1.dims != f2.dims:
@@ -417,8 +423,10 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
     state = SparseVolumeState(f1, spec, block, pm1, pyr, levels, cache_enabled, backend, mode,
                               strict)
     if mode == "tile":
+        if scratch_tiles is not None and cache_enabled:
+            raise ValueError("scratch_tiles needs cache_enabled=False")
         _setup_tile(state, tile_caps, hard_limit_bytes, tensor_cores, fuse_pyramid,
-                    pipeline_splits, ref_counters)
+                    pipeline_splits, ref_counters, scratch_tiles=scratch_tiles)
     else:
         for lv in levels:
             n_src, wpr = pm1.n_tiles, lv.words_per_row
@@ -433,7 +441,8 @@ def init_state(f1: FeatureMap, f2: FeatureMap, spec: LookupSpec, block: int = 8,
 
 def _setup_tile(state: SparseVolumeState, tile_caps, hard_limit_bytes: Optional[int],
                 tensor_cores: bool, fuse_pyramid: bool, pipeline_splits: Optional[int],
-                ref_counters: bool, batch: int = 1, pair_height: Optional[int] = None) -> None:
+                ref_counters: bool, batch: int = 1, pair_height: Optional[int] = None,
+                scratch_tiles: Optional[int] = None) -> None:
     """Tile-mode device state: descriptor, metadata, tile caches (all pairs of
     a batch), optional reference-model counters, split operands."""
     spec, levels, dev = state.spec, state.levels, state.device
@@ -462,8 +471,13 @@ def _setup_tile(state: SparseVolumeState, tile_caps, hard_limit_bytes: Optional[
     state.batch = batch
     state.n_tiles = n_tiles.value
     state.meta = torch.empty(meta_ints.value, dtype=torch.int32, device=dev)
+    if scratch_tiles is not None:
+        state.scratch_tiles = max(1, min(int(scratch_tiles), state.n_tiles))
     for lvl, lv in enumerate(levels):
-        lv.cache = torch.empty(per_level[lvl], dtype=torch.float32, device=dev)
+        n = per_level[lvl]
+        if state.scratch_tiles:
+            n = n // state.n_tiles * state.scratch_tiles
+        lv.cache = torch.empty(n, dtype=torch.float32, device=dev)
     _lib.call("cvb_partial_reset", _lib.C.byref(desc), _lib.ptr(state.meta), stream_handle())
     if ref_counters:
         if batch > 1:
@@ -774,6 +788,31 @@ def _range_descs(state: SparseVolumeState, splits: int):
     return state._desc_cache[key]
 
 
+def _sample_scratch_ranges(state: SparseVolumeState, centroids: CentroidField, flags: int,
+                           out: torch.Tensor) -> None:
+    """Cache-off iteration over ranges of `scratch_tiles` tiles: each range is
+    contracted into the scratch windows and gathered before the next range
+    reuses them (stream order).  The kernels address the cache by global tile
+    index, so each range passes the scratch base shifted back by its first
+    tile (only offsets inside the scratch are dereferenced)."""
+    r = state.scratch_tiles
+    f2s = _lib.ptr_array([state.pyramid.levels[l].values for l in range(state.spec.levels)])
+    per_tile = [lv.cache.numel() // r for lv in state.levels]
+    full = state.desc
+    try:
+        for t0 in range(0, state.n_tiles, r):
+            d = _lib.PartialDesc()
+            _lib.C.pointer(d)[0] = full
+            d.tile_begin, d.tile_end = t0, min(t0 + r, state.n_tiles)
+            state.desc = d
+            caches = (_lib.C.c_void_p * len(state.levels))(
+                *[lv.cache.data_ptr() - 4 * t0 * pt for lv, pt in zip(state.levels, per_tile)])
+            _contract(state, centroids, flags, f2s, caches)
+            _gather(state, centroids, flags, f2s, caches, out)
+    finally:
+        state.desc = full
+
+
 def _sample_tile_mode(state: SparseVolumeState, centroids: CentroidField,
                       out: torch.Tensor) -> None:
     """Contract then gather.  On the tensor-core path the frame is cut into
@@ -785,6 +824,9 @@ def _sample_tile_mode(state: SparseVolumeState, centroids: CentroidField,
     flags = coords_flags(centroids, state.strict)
     if not state.cache_enabled:
         flags |= _lib.CVB_NO_CACHE
+    if state.scratch_tiles:
+        _sample_scratch_ranges(state, centroids, flags, out)
+        return
     f2s, caches = _contract_args(state, centroids, flags)
     splits = state.pipeline_splits
     if splits <= 1:

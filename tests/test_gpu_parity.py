@@ -162,6 +162,29 @@ def test_dense_strict_bit_exact(golden, cuda, name):
 
 
 @pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("mode", ["pool_features", "pool_volume"])
+def test_dense_tc_volume_within_gates(golden, cuda, name, mode):
+    """Fast dense volume (tcgen05 split-fp16, cvb_dense_tc): every level matrix
+    within the north-star gate of the strict (reference-exact) volume, and
+    lookups within both gates of the reference outputs."""
+    spec = _spec(golden, name)
+    f1, f2, coords, outs = _case(golden, name, cuda)
+    fast = cvb.build_volume_pyramid(f1, f2, spec.levels, mode=mode)
+    strict = cvb.build_volume_pyramid(f1, f2, spec.levels, mode=mode, strict=True)
+    n1 = float(torch.linalg.vector_norm(f1.values, dim=-1).max())
+    n2 = float(torch.linalg.vector_norm(f2.values, dim=-1).max())
+    for a, b in zip(fast.level_mats, strict.level_mats):
+        assert a.shape == b.shape
+        if a.numel():
+            assert float((a - b).abs().max()) <= NS_GATE * n1 * n2
+    if mode == "pool_features":
+        for c, want in zip(coords, outs):
+            got = cvb.lookup_dense(fast, c, spec).numpy()
+            ref_dev, ns_dev = _gates(got, want, golden[f"{name}/f1"], golden[f"{name}/f2"])
+            assert ref_dev <= REF_GATE and ns_dev <= NS_GATE, (ref_dev, ns_dev)
+
+
+@pytest.mark.parametrize("name", CASES)
 @pytest.mark.parametrize("mode", ["tile", "block"])
 def test_partial_strict_bit_exact(golden, cuda, name, mode):
     spec = _spec(golden, name)
