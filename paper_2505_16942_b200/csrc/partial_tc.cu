@@ -220,11 +220,10 @@ struct TcParams {
   int dbg;                             // profiling knockouts (CVB_TC_DEBUG; debug instantiation only)
   unsigned long long* ts;              // role timeline (CVB_TC_DEBUG & 16; debug instantiation only)
   int* watchdog;                       // host-mapped error word (null: none); see wait_phase
-  // dense mode (cvb_dense_tc): every tile's "new cells" are all cells of every
-  // level and the epilogue writes the all-pairs rows dense[l][pixel][cell]
-  // instead of cache slots
+  // dense instantiation (cvb_dense_tc): every tile's "new cells" are all cells
+  // of every level and the epilogue writes the all-pairs rows
+  // dense[l][pixel][cell] instead of cache slots
   float* dense[CVB_MAX_LEVELS];
-  int dense_mode;
 };
 
 // Operand preparation, once per image pair.  Every row (a query of F1, a
@@ -546,7 +545,7 @@ __device__ __forceinline__ void stamp(const tc::TcParams& T, int64_t it, int e) 
 
 // DEBUG=false is the production instantiation: the CVB_TC_DEBUG knock-outs
 // and the %globaltimer role timeline compile out of it.
-template <bool DEBUG>
+template <bool DEBUG, bool DENSE = false>
 __global__ void __launch_bounds__(THREADS, 1)
     partial_contract_tcp_kernel(const __grid_constant__ tc::TcParams T) {
   extern __shared__ uint8_t smem_raw[];
@@ -780,7 +779,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int n = S.n_cells;
       const int n_chunks = (n + tc::M - 1) / tc::M;
       const int64_t pair = P.batch > 1 ? tile / P.tiles_pp : 0;
-      const TileRef tr = tile_ref(P, tile);
+      const TileRef tr = DENSE ? tile_ref(P, tile) : TileRef{0, 0, 0, 0};
       if (n_chunks > 0) {
         // the tile's 64 query scales 2^-e_q
         tc::named_bar(1, 128);
@@ -798,7 +797,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         int e_c = 0;
         if (gi < n) {
           const tc::CellRef cr = tc::cell_of(gi, S.plan, S.prefix, P.levels);
-          if (T.dense_mode) {
+          if (DENSE) {
             plane = (int64_t)P.th[cr.level] * P.tw[cr.level];  // row length of the level
             dd = T.dense[cr.level] + (int64_t)cr.cy * P.tw[cr.level] + cr.cx;
           } else {
@@ -838,7 +837,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               const int g = (2 * h + r) * 2 + c;  // == qgroup(4h + 2r, 4c)
               tc::st_global_v8(dst + g * plane, o);
             }
-          } else if (dd != nullptr) {
+          } else if (DENSE && dd != nullptr) {
             // dense rows: query q of the tile -> pixel (8ty + q/8, 8tx + q%8); a
             // warp's lanes are consecutive cells, so each store is 128 B
 #pragma unroll 4
@@ -1230,7 +1229,6 @@ int cvb_dense_tc(const cvb_partial_desc* desc, const void* f1_split,
     T.e2[l] = reinterpret_cast<const int8_t*>(T.f2s[l] + 2 * T.plane[l]);
     T.dense[l] = out_levels_host[l];
   }
-  T.dense_mode = 1;
   cudaStream_t s = as_stream(stream);
   int* word = tcp::watchdog_word(s);
   T.watchdog = word != nullptr ? tcp::watchdog_dev : nullptr;
@@ -1239,13 +1237,13 @@ int cvb_dense_tc(const cvb_partial_desc* desc, const void* f1_split,
   const int n_sms = tcp::sm_count(dev);
   const size_t smem = tcp::smem_bytes();
   static std::atomic<uint64_t> attr{0};
-  ensure_max_smem(attr, tcp::partial_contract_tcp_kernel<false>, (int)smem);
+  ensure_max_smem(attr, tcp::partial_contract_tcp_kernel<false, true>, (int)smem);
   tcp::dense_plan_kernel<<<(unsigned)ceil_div(P.n_tiles, 128), 128, 0, s>>>(P);
   int st = check_launch("dense_plan");
   if (st != CVB_OK) return st;
   const int64_t grid = P.ntile < n_sms ? P.ntile : n_sms;
-  launch_pdl(tcp::partial_contract_tcp_kernel<false>, dim3((unsigned)grid), dim3(tcp::THREADS),
-             smem, s, T);
+  launch_pdl(tcp::partial_contract_tcp_kernel<false, true>, dim3((unsigned)grid),
+             dim3(tcp::THREADS), smem, s, T);
   return check_launch("dense_tc");
 }
 
