@@ -17,6 +17,21 @@ for variant, kw in [("partial", {}), ("partial", {"strict": True}), ("partial", 
     s = cvb.CorrSampler(f1, f2, spec, variant=variant, **kw)
     for c in cents:
         s(c)
+# batched tile path (fast + strict), reference-model counters, stateless scratch ranges
+b1 = torch.stack([f1.values, f1.values.flip(0).contiguous()])
+b2 = torch.stack([f2.values, f2.values.flip(1).contiguous()])
+bc = [torch.stack([c.coords, c.coords]) for c in cents]
+for strict in (False, True):
+    bs = cvb.BatchCorrSampler(b1, b2, spec, strict=strict, graph=False)
+    for c in bc:
+        bs(c)
+st = cvb.init_state(f1, f2, spec, 4, ref_counters=True)
+for c in cents:
+    cvb.sample_iteration(st, c)
+st.counter.blocks_computed
+st = cvb.init_state(f1, f2, spec, cache_enabled=False, scratch_tiles=3)
+for c in cents:
+    cvb.sample_iteration(st, c)
 blk = cvb.CorrBlock(f1.values.permute(2, 0, 1)[None].contiguous(), f2.values.permute(2, 0, 1)[None].contiguous(),
                     num_levels=3, radius=4)
 blk(torch.from_numpy(np.ascontiguousarray(sc.centroid_fields[1].transpose(2, 0, 1)))[None].to(dev))
