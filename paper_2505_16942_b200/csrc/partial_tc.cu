@@ -453,8 +453,14 @@ __device__ __forceinline__ CellRef cell_of(int g, const TilePlan* plans, const i
 // ---------------------------------------------------------------------------
 namespace tcp {
 
-constexpr int NST = 4;              // A stages (32 KB each: hi + lo, 128 rows x 64 channels)
-constexpr int NBP = 5;              // F1 pieces in the ring (16 KB each)
+#ifndef CVB_TC_NST
+#define CVB_TC_NST 4
+#endif
+#ifndef CVB_TC_NBP
+#define CVB_TC_NBP 5
+#endif
+constexpr int NST = CVB_TC_NST;     // A stages (32 KB each: hi + lo, 128 rows x 64 channels)
+constexpr int NBP = CVB_TC_NBP;     // F1 pieces in the ring (16 KB each)
 constexpr int NPL = 4;              // plan slots
 constexpr int THREADS = 512;
 constexpr int A_WARPS = 8;             // A producers: warps 4-7 and 12-15
