@@ -31,7 +31,7 @@ namespace gfast {
 // resident warps per SM as whole-tile CTAs (registers bind at 126), but small
 // CTAs retire and refill independently (-6% sampler time at C4)
 constexpr int WARPS = 2;
-constexpr int CTAS_PER_TILE = (TQ / QG) / WARPS;  // 8 query groups per tile
+constexpr int CTAS_PER_TILE = (TQ / QG) / WARPS;  // 8 query groups per tile, one quad per CTA
 constexpr int MAXL = 4;    // levels per launch
 constexpr int R = 4, K = 9, KK = 81, S = 10;
 
@@ -111,8 +111,10 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
   const int64_t tile = P.tile0 + blockIdx.x / CTAS_PER_TILE;
   const TileRef tr = tile_ref(P, tile);
   const int tile_y = tr.ty, tile_x = tr.tx;
-  // query group: tile rows 2(g>>1)..+1, columns 4(g&1)..+3
-  const int grp = (int)(blockIdx.x % CTAS_PER_TILE) * WARPS + warp;
+  // the CTA's two warps take the two groups of one quad (tile rows
+  // 4(c>>1)..+3, columns 4(c&1)..+3), so they share every cache line
+  const int quad = (int)(blockIdx.x % CTAS_PER_TILE);
+  const int grp = (2 * (quad >> 1) + warp) * 2 + (quad & 1);
   const int py0 = tile_y * TQH + group_qy(grp, 0), px0 = tile_x * TQW + group_qx(grp, 0);
   if (py0 >= P.h1) return;  // warp-uniform
 
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
   if (li < nlev && qvalid && status != ST_OVERFLOW) {
     const int l = level0 + li;
     const int th = P.th[l], tw = P.tw[l], ch = P.ch[l], cw = P.cw[l];
-    const float* plane = P.cache[l] + ((tile * QG + grp) * (int64_t)(ch * cw)) * QG + q;
+    const float* plane = P.cache[l] + tile * (int64_t)(ch * cw) * TQ + cache_off(grp, 0, ch * cw, q);
     const int x0 = ax - R;
     int xs = x0 % cw;
     if (xs < 0) xs += cw;
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
     bool colin[S];
 #pragma unroll
     for (int i = 0; i < S; ++i) {
-      colofs[i] = xs * QG;
+      colofs[i] = xs * QUAD_F;
       colin[i] = x0 + i >= 0 && x0 + i < tw;
       if (++xs == cw) xs = 0;
     }
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
         if (pass > 0 && j == 0) continue;
         const int gy = y0 + j;
         const bool rin = status == ST_OK && gy >= 0 && gy < th;
-        const float* prow = plane + (int64_t)(sy * cw) * QG;
+        const float* prow = plane + (int64_t)(sy * cw) * QUAD_F;
 #pragma unroll
         for (int i = 0; i < S; ++i) v[j][i] = (rin && colin[i]) ? __ldg(prow + colofs[i]) : 0.f;
         if (++sy == ch) sy = 0;
