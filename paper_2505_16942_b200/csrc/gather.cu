@@ -7,11 +7,10 @@
 // levels pipeline: while level l's taps are combined, level l+1's cache region
 // is already in flight.
 //   * staging: the union of the 8 supports of a level is a rectangle of
-//     cells; in the warp's quad plane ([slot][2 halves][8 queries], 64 B per
-//     cell, partial.cuh) every in-grid row of it is one contiguous run of
-//     slots (two if it wraps the toroidal column), fetched with one
-//     cp.async.bulk per run into a double-buffered shared-memory region (both
-//     halves: the lines are fetched whole anyway); cells outside the grid are
+//     cells; in the warp's cache plane ([slot][8 queries], 32 B per cell)
+//     every in-grid row of it is one contiguous run of slots (two if it wraps
+//     the toroidal column), fetched with one cp.async.bulk per run into a
+//     double-buffered shared-memory region; cells outside the grid are
 //     zero-filled (dots with the zero padding, layout.py:1-14);
 //   * taps: one (query, tap row) per lane-iteration; the two region rows a tap
 //     row needs are read once and combined in registers with the canonical
@@ -32,7 +31,7 @@ namespace gather {
 
 constexpr int WARPS = 4;
 constexpr int MAXL = 4;          // levels per launch (the host loops for more)
-constexpr int REG_CELLS = 224;   // per region buffer: 224 cells x 16 floats (a quad slot) = 14 KB
+constexpr int REG_CELLS = 224;   // per region buffer: 224 cells x 8 queries x 4 B = 7 KB
 constexpr int MAX_TAPS = 81;     // r <= 4 for the staged-output path
 
 struct QInfo {
@@ -42,7 +41,7 @@ struct QInfo {
 };
 
 struct Shared {
-  float region[WARPS][2][REG_CELLS * QUAD_F];
+  float region[WARPS][2][REG_CELLS * TQW];
   float outs[WARPS][TQW * MAX_TAPS];
   QInfo q[WARPS][MAXL][TQW];
   int status[WARPS][MAXL];
@@ -109,7 +108,7 @@ __device__ __forceinline__ bool stage_region(float* R, uint32_t bar, const float
   const bool full = any && gy0 == ylo && gy1 == yhi && gx0 == xlo && gx1 == xhi;
   if (!full) {
     float4* z = reinterpret_cast<float4*>(R);
-    for (int i = lane; i < rh * rw * (QUAD_F / 4); i += 32) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = lane; i < rh * rw * 2; i += 32) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
@@ -117,7 +116,7 @@ __device__ __forceinline__ bool stage_region(float* R, uint32_t bar, const float
   const int nrow = gy1 - gy0 + 1, ncol = gx1 - gx0 + 1;
   if (lane == 0)
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                 "r"((uint32_t)(nrow * ncol * QUAD_F * 4))
+                 "r"((uint32_t)(nrow * ncol * TQW * 4))
                  : "memory");
   __syncwarp();
   // In-grid cells of the region lie in the tile box (<= cap): slot = first
@@ -128,19 +127,18 @@ __device__ __forceinline__ bool stage_region(float* R, uint32_t bar, const float
   for (int i = lane; i < nrow; i += 32) {
     int srow = ym + i;
     if (srow >= ch) srow -= ch;
-    const uint32_t dst = rbase + (uint32_t)(((gy0 - ylo + i) * rw + (gx0 - xlo)) * QUAD_F * 4);
-    bulk_copy(dst, plane + (int64_t)(srow * cw + xm) * QUAD_F, (uint32_t)(n1 * QUAD_F * 4), bar);
+    const uint32_t dst = rbase + (uint32_t)(((gy0 - ylo + i) * rw + (gx0 - xlo)) * TQW * 4);
+    bulk_copy(dst, plane + (int64_t)(srow * cw + xm) * TQW, (uint32_t)(n1 * TQW * 4), bar);
     if (ncol > n1)
-      bulk_copy(dst + (uint32_t)(n1 * QUAD_F * 4), plane + (int64_t)(srow * cw) * QUAD_F,
-                (uint32_t)((ncol - n1) * QUAD_F * 4), bar);
+      bulk_copy(dst + (uint32_t)(n1 * TQW * 4), plane + (int64_t)(srow * cw) * TQW,
+                (uint32_t)((ncol - n1) * TQW * 4), bar);
   }
   return true;
 }
 
-// Taps of the queries in `todo` from a staged region (cells of QUAD_F floats;
-// this group's values at offset `half`) into outs[q][K*K].
+// Taps of the queries in `todo` from a staged region into outs[q][K*K].
 template <bool STRICT, int K_>
-__device__ __forceinline__ void region_taps(const float* __restrict__ R, int half, const QInfo* qi,
+__device__ __forceinline__ void region_taps(const float* __restrict__ R, const QInfo* qi,
                                             unsigned todo, int ylo, int xlo, int rw, int r, int K,
                                             float scale, bool normalize, float* __restrict__ O,
                                             int lane) {
@@ -148,9 +146,8 @@ __device__ __forceinline__ void region_taps(const float* __restrict__ R, int hal
   for (int e = lane; e < TQW * K; e += 32) {
     const int q = e & (TQW - 1), dy = e >> 3;
     if (!((todo >> q) & 1u)) continue;
-    const float* a =
-        R + ((qi[q].ay - r - ylo + dy) * rw + (qi[q].ax - r - xlo)) * QUAD_F + half + q;
-    const float* b = a + rw * QUAD_F;
+    const float* a = R + ((qi[q].ay - r - ylo + dy) * rw + (qi[q].ax - r - xlo)) * TQW + q;
+    const float* b = a + rw * TQW;
     const Weights32 w32 = qi[q].w32;
     Weights64 w64;
     if (STRICT) w64 = weights64(qi[q].fx, qi[q].fy);
@@ -159,7 +156,7 @@ __device__ __forceinline__ void region_taps(const float* __restrict__ R, int hal
     if (K_ > 0) {
 #pragma unroll
       for (int i = 0; i < K_; ++i) {
-        const float a1 = a[(i + 1) * QUAD_F], b1 = b[(i + 1) * QUAD_F];
+        const float a1 = a[(i + 1) * TQW], b1 = b[(i + 1) * TQW];
         float v = STRICT ? combine64(a0, a1, b0, b1, w64) : combine32(a0, a1, b0, b1, w32);
         if (normalize) v = __fmul_rn(v, scale);
         o[i] = v;
@@ -168,7 +165,7 @@ __device__ __forceinline__ void region_taps(const float* __restrict__ R, int hal
       }
     } else {
       for (int i = 0; i < K; ++i) {
-        const float a1 = a[(i + 1) * QUAD_F], b1 = b[(i + 1) * QUAD_F];
+        const float a1 = a[(i + 1) * TQW], b1 = b[(i + 1) * TQW];
         float v = STRICT ? combine64(a0, a1, b0, b1, w64) : combine32(a0, a1, b0, b1, w32);
         if (normalize) v = __fmul_rn(v, scale);
         o[i] = v;
@@ -267,11 +264,9 @@ __global__ void __launch_bounds__(WARPS * 32)
   float* O = sm.outs[warp];
   uint32_t phase0 = 0u, phase1 = 0u;
 
-  // the group's quad plane (both halves; this group's values at +half)
-  const int half = group_half(grp) * QG;
   auto plane_of = [&](int l) {
     const int64_t cap = (int64_t)P.ch[l] * P.cw[l];
-    return P.cache[l] + tile * cap * TQ + cache_off(grp, 0, (int)cap, 0) - half;
+    return P.cache[l] + (tile * QG + grp) * cap * QG;
   };
 
   // issue the staged region of level index li into buffer b
@@ -317,7 +312,7 @@ __global__ void __launch_bounds__(WARPS * 32)
           bar_wait(bar, ph);
           ph ^= 1u;
         }
-        region_taps<STRICT, K_>(R, half, qi, todo, ylo, xlo, rw, r, K, P.scale, P.normalize, O, lane);
+        region_taps<STRICT, K_>(R, qi, todo, ylo, xlo, rw, r, K, P.scale, P.normalize, O, lane);
         __syncwarp();
         write_outs<KK_>(O, todo, out, pix0, P.w1, P.levels, l, KK, lane);
         __syncwarp();
@@ -335,7 +330,7 @@ __global__ void __launch_bounds__(WARPS * 32)
         float v = 0.f;
         if (cy >= 0 && cy < th && cx >= 0 && cx < tw) {
           if (status == ST_OK) {
-            v = __ldg(plane + (int64_t)slot_of(cy, cx, ch, cw) * QUAD_F + half + q);
+            v = __ldg(plane + (int64_t)slot_of(cy, cx, ch, cw) * TQW + q);
           } else if (status == ST_OVERFLOW) {
             const float* bb = f2 + ((int64_t)cy * tw + cx) * d;
             float acc = 0.f;
@@ -376,7 +371,7 @@ __global__ void __launch_bounds__(WARPS * 32)
         bar_wait(b ? bar1 : bar0, ph);
         ph ^= 1u;
       }
-      region_taps<STRICT, K_>(sm.region[warp][b], half, sm.q[warp][li], vmask, g.ylo, g.xlo, g.rw, r,
+      region_taps<STRICT, K_>(sm.region[warp][b], sm.q[warp][li], vmask, g.ylo, g.xlo, g.rw, r,
                               K, P.scale, P.normalize, O, lane);
       __syncwarp();
       write_outs<KK_>(O, vmask, out, pix0, P.w1, P.levels, level0 + li, KK, lane);

@@ -31,7 +31,7 @@ namespace gfast {
 // resident warps per SM as whole-tile CTAs (registers bind at 126), but small
 // CTAs retire and refill independently (-6% sampler time at C4)
 constexpr int WARPS = 2;
-constexpr int CTAS_PER_TILE = (TQ / QG) / WARPS;  // 8 query groups per tile, one quad per CTA
+constexpr int CTAS_PER_TILE = (TQ / QG) / WARPS;  // 8 query groups per tile
 constexpr int MAXL = 4;    // levels per launch
 constexpr int R = 4, K = 9, KK = 81, S = 10;
 
@@ -111,10 +111,8 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
   const int64_t tile = P.tile0 + blockIdx.x / CTAS_PER_TILE;
   const TileRef tr = tile_ref(P, tile);
   const int tile_y = tr.ty, tile_x = tr.tx;
-  // the CTA's two warps take the two groups of one quad (tile rows
-  // 4(c>>1)..+3, columns 4(c&1)..+3), so they share every cache line
-  const int quad = (int)(blockIdx.x % CTAS_PER_TILE);
-  const int grp = (2 * (quad >> 1) + warp) * 2 + (quad & 1);
+  // query group: tile rows 2(g>>1)..+1, columns 4(g&1)..+3
+  const int grp = (int)(blockIdx.x % CTAS_PER_TILE) * WARPS + warp;
   const int py0 = tile_y * TQH + group_qy(grp, 0), px0 = tile_x * TQW + group_qx(grp, 0);
   if (py0 >= P.h1) return;  // warp-uniform
 
@@ -158,7 +156,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
   if (li < nlev && qvalid && status != ST_OVERFLOW) {
     const int l = level0 + li;
     const int th = P.th[l], tw = P.tw[l], ch = P.ch[l], cw = P.cw[l];
-    const float* plane = P.cache[l] + tile * (int64_t)(ch * cw) * TQ + cache_off(grp, 0, ch * cw, q);
+    const float* plane = P.cache[l] + ((tile * QG + grp) * (int64_t)(ch * cw)) * QG + q;
     const int x0 = ax - R;
     int xs = x0 % cw;
     if (xs < 0) xs += cw;
@@ -167,7 +165,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
     bool colin[S];
 #pragma unroll
     for (int i = 0; i < S; ++i) {
-      colofs[i] = xs * QUAD_F;
+      colofs[i] = xs * QG;
       colin[i] = x0 + i >= 0 && x0 + i < tw;
       if (++xs == cw) xs = 0;
     }
@@ -189,7 +187,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
         if (pass > 0 && j == 0) continue;
         const int gy = y0 + j;
         const bool rin = status == ST_OK && gy >= 0 && gy < th;
-        const float* prow = plane + (int64_t)(sy * cw) * QUAD_F;
+        const float* prow = plane + (int64_t)(sy * cw) * QG;
 #pragma unroll
         for (int i = 0; i < S; ++i) v[j][i] = (rin && colin[i]) ? __ldg(prow + colofs[i]) : 0.f;
         if (++sy == ch) sy = 0;
@@ -253,13 +251,21 @@ int launch_gather_fast_r4(const PartialParams& P, float* out, cudaStream_t s) {
   static std::atomic<uint64_t> attr{0};
   const int smem = (int)sizeof(gfast::Shared);
   ensure_max_smem(attr, gfast::gather_fast_kernel, smem);
-  static int carve = -2;  // experiment knob: CVB_GF_CARVEOUT (percent of the unified array as smem)
-  if (carve == -2) {
+  // Shared-memory carveout 65%: the taps re-read each cache sector ~3x through
+  // L1, so L1 capacity matters more than the last CTA slot per SM (measured:
+  // 65% is 1-2% faster than the default 200 KB carveout; 100% halves the
+  // speed).  CVB_GF_CARVEOUT overrides (percent; -1 = driver default).
+  static std::atomic<uint64_t> carved{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(carved.load() & bit)) {
     const char* e = getenv("CVB_GF_CARVEOUT");
-    carve = e ? atoi(e) : -1;
+    const int carve = e ? atoi(e) : 65;
     if (carve >= 0)
       cudaFuncSetAttribute(gfast::gather_fast_kernel,
                            cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+    carved.fetch_or(bit);
   }
   for (int l0 = 0; l0 < P.levels; l0 += gfast::MAXL) {
     const int nl = min(gfast::MAXL, P.levels - l0);

@@ -83,8 +83,9 @@ __global__ void __launch_bounds__(GEMM_THREADS) partial_contract_kernel(PartialP
       // queries ty*4..ty*4+3: tile row ty>>1, columns (ty&1)*4..+3 -> one
       // group, 4 consecutive group indices (cache layout [group][slot][8])
       const int qy = ty >> 1, qx0 = (ty & 1) * 4;
-      *reinterpret_cast<float4*>(cache + cache_off(qgroup(qy, qx0), slot_of(cy, cx, ch, cw),
-                                                   ch * cw, qindex(qy, qx0))) = v;
+      *reinterpret_cast<float4*>(
+          cache + ((int64_t)qgroup(qy, qx0) * (ch * cw) + slot_of(cy, cx, ch, cw)) * QG +
+          qindex(qy, qx0)) = v;
     }
   }
 }

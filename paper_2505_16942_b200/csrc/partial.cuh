@@ -9,24 +9,12 @@ namespace cvb {
 constexpr int TQH = CVB_TILE_H, TQW = CVB_TILE_W, TQ = TQH * TQW;  // 64 queries
 constexpr int ST_OK = 0, ST_OVERFLOW = 1, ST_EMPTY = 2;
 
-// Tile-cache layout.  A query group is 2 query rows x 4 query columns of the
-// tile (8 queries, one 32-byte sector per cell); a quad is the two groups
-// stacked vertically (4 rows x 4 columns).  Per level:
-//   [tile][4 quads][cap_h * cap_w slots][2 halves (upper / lower group)][8 queries]
-// so each cached cell holds a quad's 16 costs in one 64-byte sector pair.
-// B200's L2 fills from DRAM in whole 128-byte lines (profiles/r02/
-// dram_granularity.txt), so what a sampler's window rows cost is lines, not
-// sectors: the two groups of a quad are sampled by the two warps of one CTA
-// and share every line they touch (4x4 quads: 11% fewer DRAM lines at C4
-// than 2x4 groups in separate planes).
+// Tile-cache sectors: each cached cell holds its 64 query costs as 8 groups of
+// 8 (32 bytes), a group being 2 query rows x 4 query columns of the tile.  A
+// sampler reading one group's windows fetches the union of 8 windows shifted
+// by (0..1, 0..3) cells — 10-13% fewer sectors than 8 queries of one row.
+// Cache layout per level: [tile][group][cap_h * cap_w slots][8 queries].
 constexpr int QG = 8;
-constexpr int QUAD_F = 2 * QG;  // floats per slot of a quad
-__host__ __device__ __forceinline__ int group_quad(int g) { return ((g >> 2) << 1) | (g & 1); }
-__host__ __device__ __forceinline__ int group_half(int g) { return (g >> 1) & 1; }
-// float offset of (group g, slot, query i of the group) within a tile-level block
-__host__ __device__ __forceinline__ int64_t cache_off(int g, int slot, int cap_slots, int i) {
-  return ((int64_t)group_quad(g) * cap_slots + slot) * QUAD_F + group_half(g) * QG + i;
-}
 __host__ __device__ __forceinline__ int qgroup(int qy, int qx) { return (qy >> 1) * 2 + (qx >> 2); }
 __host__ __device__ __forceinline__ int qindex(int qy, int qx) { return (qy & 1) * 4 + (qx & 3); }
 __host__ __device__ __forceinline__ int group_qy(int g, int i) { return 2 * (g >> 1) + (i >> 2); }

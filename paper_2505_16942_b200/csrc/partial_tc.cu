@@ -808,9 +808,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             dd = T.dense[cr.level] + (int64_t)cr.cy * P.tw[cr.level] + cr.cx;
           } else {
             const int ch = P.ch[cr.level], cw = P.cw[cr.level];
-            plane = (int64_t)ch * cw * QUAD_F;  // floats per quad plane
-            dst = P.cache[cr.level] + tile * plane * 4 +
-                  (int64_t)slot_of(cr.cy, cr.cx, ch, cw) * QUAD_F;
+            plane = (int64_t)ch * cw * TQW;
+            dst = P.cache[cr.level] + tile * plane * TQH +
+                  (int64_t)slot_of(cr.cy, cr.cx, ch, cw) * TQW;
           }
           e_c = T.e2[cr.level][pair * T.pair_bytes[cr.level] + (int64_t)cr.cy * P.tw[cr.level] + cr.cx];
         }
@@ -824,9 +824,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc::tmem_ld32(tmem + ab * 128 + lane_base + h * 32, vm);
           tc::tmem_ld32(tmem + ab * 128 + 64 + lane_base + h * 32, vc);
           if (dst != nullptr && !(DEBUG && (T.dbg & 2))) {
-            // this half holds tile rows 4h..4h+3 = quads 2h, 2h+1; each group's 8
-            // costs (32 B, one sector) leave in one 256-bit store, so a warp
-            // writes whole sectors of consecutive slots
+            // this half holds tile rows 4h..4h+3 = query groups 4h/2*2 .. +3;
+            // each group's 8 costs (32 B, one cache sector) leave in one
+            // 256-bit store, so a warp writes whole sectors of consecutive slots
 #pragma unroll
             for (int gg = 0; gg < 4; ++gg) {
               const int r = gg >> 1, c = gg & 1;  // row pair and column half in this half
@@ -840,9 +840,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 o[4 + i] = fmaf(vc[j1 + i], 1.f / (1 << tc::LOG2_LO), vm[j1 + i]) *
                            (s_q[h * 32 + j1 + i] * s_c);
               }
-              // group (2h + r, c) = half r of quad 2h + c: the two halves of a
-              // quad are adjacent 32-byte sectors of one 64-byte slot
-              tc::st_global_v8(dst + (2 * h + c) * plane + r * QG, o);
+              const int g = (2 * h + r) * 2 + c;  // == qgroup(4h + 2r, 4c)
+              tc::st_global_v8(dst + g * plane, o);
             }
           } else if (DENSE && dd != nullptr) {
             // dense rows: query q of the tile -> pixel (8ty + q/8, 8tx + q%8); a

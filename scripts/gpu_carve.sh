@@ -1,6 +1,6 @@
 cd ${GRAFT_REPO_ROOT:-.}
 mkdir -p gpurun_out
-for C in -1 80 70 60 50 40; do
+for C in -1 70 60 100; do
   CVB_GF_CARVEOUT=$C timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-compare --no-e2e > gpurun_out/carve_$C.json 2>/dev/null
   python -c "
 import json,statistics
