@@ -57,6 +57,11 @@ typedef enum {
                                  channel-first [L * (2r+1)^2][H][W], window index
                                  dx * (2r+1) + dy (fast r=4 sampler only) */
 
+#define CVB_TC_PAIRS 64        /* cvb_partial_contract_tc: contract on SM pairs
+                                 (tcgen05.mma.cta_group::2, two adjacent tiles'
+                                 box hull per pair) — for cold iterations
+                                 (the first after a reset, or CVB_NO_CACHE);
+                                 needs a range of whole tile rows, else ignored */
 #define CVB_MAX_LEVELS 8
 
 /* ---- library ------------------------------------------------------------ */

@@ -29,6 +29,7 @@ CVB_NO_CACHE = 4
 CVB_PREP_POOL = 8
 CVB_OUT_RAFT = 16
 CVB_ACCESS_NO_TRIM = 32
+CVB_TC_PAIRS = 64
 
 MAX_LEVELS = 8
 TILE_H = 8

@@ -1088,6 +1088,512 @@ int* watchdog_word(cudaStream_t s) {
 
 }  // namespace tcp
 
+// ---------------------------------------------------------------------------
+// Cold-iteration contraction on SM pairs (tcgen05.mma.cta_group::2).
+//
+// At iteration 0 (and every iteration with the cache off) each tile contracts
+// its whole bounding box, and horizontally adjacent tiles' boxes share most of
+// their cells: gathering every tile's A rows separately moves 6.2 GB through
+// L2 -> SMEM at C4, the cold contraction's limit.  Here a cluster of two CTAs
+// (one SM pair) takes a PAIR of horizontally adjacent tiles and contracts the
+// hull of their two boxes once, as M=256 chunks: each CTA gathers half of
+// every chunk's cell rows (A) and holds its own tile's F1 image (B = the two
+// tiles' 128 queries, N-split across the CTAs); the leader CTA issues
+// tcgen05.mma.cta_group::2 (main = A_hi.B_hi, corr = A_hi.B_lo + A_lo.B_hi,
+// three N=128 MMAs per K=16 step) and every commit is multicast to both
+// CTAs' barriers.  Each CTA's TMEM holds its 128 cells x 128 queries; its
+// epilogue writes every cell that lies in tile j's box into tile j's cache
+// (the same cells the single-tile kernel writes when the tile is cold; a
+// cell of the previous box is rewritten with its own value when it is not).
+// Cross-CTA signalling: the follower's A / B completions are relayed by its
+// warp 1 to the leader's full barriers; the follower's epilogue arrives on
+// the leader's accumulator-empty barrier remotely.
+// ---------------------------------------------------------------------------
+namespace tcp2 {
+
+using tcp::NST;
+using tcp::NBP;
+using tcp::NPL;
+using tcp::THREADS;
+using tcp::A_WARPS;
+using tcp::A_ROWS;
+
+constexpr int M2 = 256;  // cells per pair chunk (128 per CTA)
+constexpr int RELAY_LANES = NST + 1;  // follower relay: one lane per A stage + one for B
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// Relaxed remote arrive: no cluster-scope membar (a release arrive costs a
+// fence per call, which serialised the relay to ~1.3 us per stage).  What it
+// publishes is already complete: cp.async data whose local barrier the relay
+// has observed (plus fence.proxy.async), or TMEM reads retired by
+// tcgen05.wait::ld + tcgen05.fence::before_thread_sync.
+__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void st_cluster_u64(uint32_t cluster_addr, unsigned long long v) {
+  asm volatile("st.relaxed.cluster.shared::cluster.u64 [%0], %1;" ::"r"(cluster_addr), "l"(v)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+template <uint32_t ID>
+__device__ __forceinline__ void mma2(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(ID), "r"(acc));
+}
+__device__ __forceinline__ void commit_mc(uint32_t mbar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(mbar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// D f32, A/B f16 K-major, N=128 (64 per CTA), M=256 (128 per CTA)
+constexpr uint32_t IDESC2 = (1u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(M2 >> 4) << 24);
+
+// Work item: a pair of horizontally adjacent tiles (tile[1] < 0: a lone last
+// tile of an odd tile row) and the per-level hull of their boxes.
+struct PairSlot {
+  PlanRec rec[2];
+  int hull[CVB_MAX_LEVELS][4];  // ylo, yhi, xlo, xhi
+  int hw[CVB_MAX_LEVELS];       // hull width
+  int prefix[CVB_MAX_LEVELS + 1];
+  int n_cells;
+  int tile[2];
+  int end;
+};
+
+struct Ctl2 {
+  uint64_t plan_full[NPL], plan_empty[NPL], plan_copy[NPL];
+  uint64_t pidx_full[NPL];         // follower: the leader posted the slot's pair index
+  unsigned long long pidx[NPL];    // follower: pair index mailbox (written by the leader)
+  uint64_t b_full[NBP], b_empty[NBP];
+  uint64_t a_full[NST], a_empty[NST];
+  uint64_t acc_full[2], acc_empty[2];
+  PairSlot slot[NPL];
+  float qscale[2 * tc::N];
+  uint32_t tmem;
+  int abort;
+};
+
+size_t smem_bytes() {
+  return (size_t)NST * tc::A_STAGE + (size_t)NBP * tc::B_PIECE + sizeof(Ctl2) + 1024;
+}
+
+__device__ __forceinline__ bool in_box(const Box& b, int y, int x) {
+  return y >= b.ylo && y <= b.yhi && x >= b.xlo && x <= b.xhi;
+}
+
+// pair index -> the two global tiles (pairs never straddle a tile row)
+__device__ __forceinline__ void pair_tiles(const PartialParams& P, int64_t pidx, int& t0, int& t1) {
+  const int ppr = (P.tiles_x + 1) / 2;  // pairs per tile row
+  const int64_t row = pidx / ppr;
+  const int pc = (int)(pidx - row * ppr);
+  const int64_t base = P.tile0 + row * P.tiles_x;  // P.tile0 is a row boundary
+  t0 = (int)(base + 2 * pc);
+  t1 = 2 * pc + 1 < P.tiles_x ? t0 + 1 : -1;
+}
+
+#define WAIT_FULL2(bar, k) tcp::wait_phase((bar), (uint32_t)(k) & 1u, &C.abort, T.watchdog)
+#define WAIT_EMPTY2(bar, k) tcp::wait_phase((bar), ((uint32_t)(k) & 1u) ^ 1u, &C.abort, T.watchdog)
+#define WAIT_FULL_CL(bar, k) tcp::wait_phase((bar), (uint32_t)(k) & 1u, &C.abort, T.watchdog)
+#define WAIT_EMPTY_CL(bar, k) tcp::wait_phase((bar), ((uint32_t)(k) & 1u) ^ 1u, &C.abort, T.watchdog)
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    pair_contract_kernel(const __grid_constant__ tc::TcParams T, int64_t n_pairs) {
+  extern __shared__ uint8_t smem_raw[];
+  const PartialParams& P = T.P;
+  const int dp = T.dp;
+  const int n_kb = dp / tc::KP;
+  const uint32_t raw = tc::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + NST * tc::A_STAGE;
+  Ctl2& C = *reinterpret_cast<Ctl2*>(sB + NBP * tc::B_PIECE);
+  const uint32_t uB = tc::smem_u32(sB), uA = tc::smem_u32(sA);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  auto U = [](const uint64_t& b) { return tc::smem_u32(&b); };
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     tc::smem_u32(&C.tmem))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  if (tid == 32) {
+    for (int i = 0; i < NPL; ++i) {
+      tc::mbar_init(U(C.plan_full[i]), 1);
+      // B producer + MMA issuer (leader) or the RELAY_LANES relay lanes
+      // (follower) + A producers + epilogue
+      tc::mbar_init(U(C.plan_empty[i]), 1 + (leader ? 1 : RELAY_LANES) + 32 * A_WARPS + 128);
+      tc::mbar_init(U(C.plan_copy[i]), 1);
+      tc::mbar_init(U(C.pidx_full[i]), 1);
+    }
+    for (int i = 0; i < NBP; ++i) {
+      tc::mbar_init(U(C.b_full[i]), leader ? 2 : 1);  // leader: own copy + the follower's relay
+      tc::mbar_init(U(C.b_empty[i]), 1);
+    }
+    for (int i = 0; i < NST; ++i) {
+      tc::mbar_init(U(C.a_full[i]), 32 * A_WARPS + (leader ? 1 : 0));
+      tc::mbar_init(U(C.a_empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(U(C.acc_full[i]), 1);
+      tc::mbar_init(U(C.acc_empty[i]), 4 + 1);  // leader: 4 local epilogue warps + the follower
+    }
+    C.abort = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc::tc_fence_after();
+  const uint32_t tmem = C.tmem;
+  pdl_trigger();
+  pdl_wait();
+
+  if (warp == 0) {
+    // ---------------- B producer: this CTA's tile's F1 pieces ----------------
+    if (lane == 0) {
+      uint32_t pb = 0;
+      for (int64_t it = 0;; ++it) {
+        const int s = (int)(it % NPL);
+        if (!WAIT_FULL2(U(C.plan_full[s]), (uint32_t)(it / NPL))) goto done;
+        const PairSlot& S = C.slot[s];
+        if (S.end) break;
+        if (S.n_cells > 0) {
+          const int my = S.tile[rank] >= 0 ? S.tile[rank] : S.tile[0];
+          const uint8_t* src = T.f1s + (int64_t)my * n_kb * tc::B_PIECE;
+          for (int q = 0; q < n_kb; ++q, ++pb) {
+            const int bs = (int)(pb % NBP);
+            if (!WAIT_EMPTY2(U(C.b_empty[bs]), pb / NBP)) goto done;
+            tc::mbar_expect_tx(U(C.b_full[bs]), tc::B_PIECE);
+            tc::bulk_g2s(uB + bs * tc::B_PIECE, src + (int64_t)q * tc::B_PIECE, tc::B_PIECE,
+                         U(C.b_full[bs]));
+          }
+        }
+        tcp::arrive(U(C.plan_empty[s]));
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      // ---------------- MMA issuer (leader CTA) ----------------
+      uint32_t pb = 0, g = 0, cg = 0;
+      for (int64_t it = 0;; ++it) {
+        const int s = (int)(it % NPL);
+        if (!__all_sync(0xffffffffu, WAIT_FULL2(U(C.plan_full[s]), (uint32_t)(it / NPL))))
+          goto done;
+        if (C.slot[s].end) break;
+        const int n = C.slot[s].n_cells;
+        if (n > 0) {
+          const int n_chunks = (n + M2 - 1) / M2;
+          for (int c = 0; c < n_chunks; ++c, ++cg) {
+            const int ab = cg & 1;
+            if (!__all_sync(0xffffffffu, WAIT_EMPTY_CL(U(C.acc_empty[ab]), cg >> 1))) goto done;
+            tc::tc_fence_after();
+            const uint32_t d_main = tmem + ab * 256, d_corr = d_main + 128;
+            for (int kb = 0; kb < n_kb; ++kb, ++g) {
+              const uint32_t pi = pb + kb;
+              const int bs = (int)(pi % NBP);
+              if (c == 0 && !__all_sync(0xffffffffu, WAIT_FULL_CL(U(C.b_full[bs]), pi / NBP)))
+                goto done;
+              const int st = (int)(g % NST);
+              if (!__all_sync(0xffffffffu, WAIT_FULL_CL(U(C.a_full[st]), g / NST))) goto done;
+              tc::tc_fence_after();
+              const uint32_t a_hi = uA + st * tc::A_STAGE, a_lo = a_hi + tc::A_HALF;
+              const uint32_t b_hi = uB + bs * tc::B_PIECE, b_lo = b_hi + tc::B_HALF;
+              const uint64_t dah = tc::make_desc_sw128(a_hi), dal = tc::make_desc_sw128(a_lo);
+              const uint64_t dbh = tc::make_desc(b_hi, 128, (tc::KP / 8) * 128);
+              const uint64_t dbl = tc::make_desc(b_lo, 128, (tc::KP / 8) * 128);
+              if (tc::elect_one()) {
+#pragma unroll
+                for (int k = 0; k < tc::KP / 16; ++k) {
+                  const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+                  mma2<IDESC2>(d_main, dah + 2 * k, dbh + 16 * k, acc);  // A_hi B_hi
+                  mma2<IDESC2>(d_corr, dah + 2 * k, dbl + 16 * k, acc);  // A_hi B_lo
+                  mma2<IDESC2>(d_corr, dal + 2 * k, dbh + 16 * k, 1u);   // A_lo B_hi
+                }
+                commit_mc(U(C.a_empty[st]));
+                if (c == n_chunks - 1) commit_mc(U(C.b_empty[bs]));
+                if (kb == n_kb - 1) commit_mc(U(C.acc_full[ab]));
+              }
+              __syncwarp();
+            }
+          }
+          pb += n_kb;
+        }
+        if (lane == 0) tcp::arrive(U(C.plan_empty[s]));
+      }
+    } else if (lane < RELAY_LANES) {
+      // ---------------- relay (follower CTA): A / B completions -> leader ----------------
+      // lane st < NST relays A stage st, lane NST the B pieces; the lanes walk
+      // the same work sequence independently, so relays of different stages
+      // overlap
+      uint32_t pb = 0, g = 0;
+      for (int64_t it = 0;; ++it) {
+        const int s = (int)(it % NPL);
+        if (!WAIT_FULL2(U(C.plan_full[s]), (uint32_t)(it / NPL))) goto done;
+        if (C.slot[s].end) break;
+        const int n = C.slot[s].n_cells;
+        if (n > 0) {
+          const int n_chunks = (n + M2 - 1) / M2;
+          for (int c = 0; c < n_chunks; ++c) {
+            for (int kb = 0; kb < n_kb; ++kb, ++g) {
+              const uint32_t pi = pb + kb;
+              const int bs = (int)(pi % NBP);
+              if (c == 0 && lane == NST) {
+                if (!WAIT_FULL2(U(C.b_full[bs]), pi / NBP)) goto done;
+                arrive_remote(mapa(U(C.b_full[bs]), 0));
+              }
+              const int st = (int)(g % NST);
+              if (lane == st) {
+                if (!WAIT_FULL2(U(C.a_full[st]), g / NST)) goto done;
+                tc::fence_proxy_async();
+                arrive_remote(mapa(U(C.a_full[st]), 0));
+              }
+            }
+          }
+          pb += n_kb;
+        }
+        tcp::arrive(U(C.plan_empty[s]));
+      }
+    }
+  } else if (warp == 2) {
+    // ---------------- plan loader: both tiles' records + the per-level hull ----------------
+    if (lane == 0) {
+      for (int64_t it = 0;; ++it) {
+        const int s = (int)(it % NPL);
+        if (!WAIT_EMPTY2(U(C.plan_empty[s]), (uint32_t)(it / NPL))) goto done;
+        PairSlot& S = C.slot[s];
+        // dynamic pair scheduling: the leader claims the next pair and posts
+        // its index into the follower's mailbox for the same slot
+        int64_t pidx;
+        if (leader) {
+          pidx = atomicAdd(tcp::tile_counter(P), 1);  // reset by plan_kernel
+          st_cluster_u64(mapa(tc::smem_u32(&C.pidx[s]), 1), (unsigned long long)pidx);
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                           mapa(U(C.pidx_full[s]), 1))
+                       : "memory");
+        } else {
+          if (!WAIT_FULL2(U(C.pidx_full[s]), (uint32_t)(it / NPL))) goto done;
+          pidx = (int64_t)*reinterpret_cast<volatile unsigned long long*>(&C.pidx[s]);
+        }
+        if (pidx >= n_pairs) {
+          S.end = 1;
+          tcp::arrive(U(C.plan_full[s]));
+          break;
+        }
+        int t0, t1;
+        pair_tiles(P, pidx, t0, t1);
+        S.end = 0;
+        S.tile[0] = t0;
+        S.tile[1] = t1;
+        const uint32_t rec_bytes = (uint32_t)sizeof(PlanRec);
+        tc::mbar_expect_tx(U(C.plan_copy[s]), rec_bytes * (t1 >= 0 ? 2 : 1));
+        tc::bulk_g2s(tc::smem_u32(&S.rec[0]), P.plans + (int64_t)t0 * PLAN_INTS, rec_bytes,
+                     U(C.plan_copy[s]));
+        if (t1 >= 0)
+          tc::bulk_g2s(tc::smem_u32(&S.rec[1]), P.plans + (int64_t)t1 * PLAN_INTS, rec_bytes,
+                       U(C.plan_copy[s]));
+        if (!WAIT_FULL2(U(C.plan_copy[s]), (uint32_t)(it / NPL))) goto done;
+        int acc = 0;
+        for (int l = 0; l < CVB_MAX_LEVELS; ++l) {
+          S.prefix[l] = acc;
+          int ylo = INT_MAX, yhi = INT_MIN, xlo = INT_MAX, xhi = INT_MIN;
+          if (l < P.levels) {
+            for (int j = 0; j < 2; ++j) {
+              if (j == 1 && t1 < 0) continue;
+              const TilePlan& tp = S.rec[j].plan[l];
+              if (tp.status != ST_OK) continue;
+              ylo = min(ylo, tp.B.ylo);
+              yhi = max(yhi, tp.B.yhi);
+              xlo = min(xlo, tp.B.xlo);
+              xhi = max(xhi, tp.B.xhi);
+            }
+          }
+          const bool any = ylo <= yhi && xlo <= xhi;
+          S.hull[l][0] = ylo;
+          S.hull[l][1] = yhi;
+          S.hull[l][2] = xlo;
+          S.hull[l][3] = xhi;
+          S.hw[l] = any ? xhi - xlo + 1 : 1;
+          acc += any ? (yhi - ylo + 1) * (xhi - xlo + 1) : 0;
+        }
+        S.prefix[CVB_MAX_LEVELS] = acc;
+        S.n_cells = acc;
+        tcp::arrive(U(C.plan_full[s]));
+      }
+    }
+  } else if ((warp >= 4 && warp < 8) || warp >= 12) {
+    // ---------------- A producers: this CTA's half of every 256-cell chunk ----------------
+    const int aw = warp < 8 ? warp - 4 : warp - 8;
+    const int sub = lane >> 3, chunk = lane & 7;
+    uint32_t g = 0;
+    for (int64_t it = 0;; ++it) {
+      const int s = (int)(it % NPL);
+      if (!__all_sync(0xffffffffu, WAIT_FULL2(U(C.plan_full[s]), (uint32_t)(it / NPL)))) goto done;
+      const PairSlot& S = C.slot[s];
+      if (S.end) break;
+      const int n = S.n_cells;
+      const int n_chunks = (n + M2 - 1) / M2;
+      const int64_t pair = P.batch > 1 ? S.tile[0] / P.tiles_pp : 0;
+      for (int c = 0; c < n_chunks; ++c) {
+        const int gi = c * M2 + (int)rank * tc::M + A_ROWS * aw + (lane % A_ROWS);
+        const __half* my_hi = nullptr;
+        int64_t my_plane = 0;
+        if (gi < n) {
+          int l = 0;
+          while (l + 1 < P.levels && gi >= S.prefix[l + 1]) ++l;
+          const int idx = gi - S.prefix[l];
+          const int cy = S.hull[l][0] + idx / S.hw[l], cx = S.hull[l][2] + idx % S.hw[l];
+          my_hi = reinterpret_cast<const __half*>(reinterpret_cast<const uint8_t*>(T.f2s[l]) +
+                                                  pair * T.pair_bytes[l]) +
+                  ((int64_t)cy * P.tw[l] + cx) * dp;
+          my_plane = T.plane[l];
+        }
+        for (int kb = 0; kb < n_kb; ++kb, ++g) {
+          const int st = (int)(g % NST);
+          if (!__all_sync(0xffffffffu, WAIT_EMPTY2(U(C.a_empty[st]), g / NST))) goto done;
+          const uint32_t stage = uA + st * tc::A_STAGE;
+#pragma unroll
+          for (int i = 0; i < A_ROWS / 4; ++i) {
+            const int rl = 4 * i + sub;
+            const __half* hi = reinterpret_cast<const __half*>(
+                __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_hi), rl));
+            const int64_t pl = __shfl_sync(0xffffffffu, my_plane, rl);
+            if (hi != nullptr) {
+              const int row = A_ROWS * aw + rl;
+              const uint32_t dst = stage + row * 128 + ((chunk ^ (row & 7)) << 4);
+              const __half* src = hi + kb * tc::KP + chunk * 8;
+              tc::cp_async16(dst, src);
+              tc::cp_async16(dst + tc::A_HALF, src + pl);
+            }
+          }
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                           U(C.a_full[st]))
+                       : "memory");
+        }
+      }
+      tcp::arrive(U(C.plan_empty[s]));
+    }
+  } else if (warp >= 8 && warp < 12) {
+    // ---------------- epilogue: this CTA's 128 cells x both tiles' queries ----------------
+    const int ep = tid - 256;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    float* s_q = &C.qscale[0];
+    const uint32_t acc_empty_l0 = mapa(U(C.acc_empty[0]), 0), acc_empty_l1 = mapa(U(C.acc_empty[1]), 0);
+    uint32_t cg = 0;
+    for (int64_t it = 0;; ++it) {
+      const int s = (int)(it % NPL);
+      if (!__all_sync(0xffffffffu, WAIT_FULL2(U(C.plan_full[s]), (uint32_t)(it / NPL)))) goto done;
+      const PairSlot& S = C.slot[s];
+      if (S.end) break;
+      const int n = S.n_cells;
+      const int n_chunks = (n + M2 - 1) / M2;
+      const int64_t pair = P.batch > 1 ? S.tile[0] / P.tiles_pp : 0;
+      if (n_chunks > 0) {
+        tc::named_bar(1, 128);
+        {
+          const int j = ep >> 6, q = ep & 63;
+          const int t = S.tile[j] >= 0 ? S.tile[j] : S.tile[0];
+          s_q[ep] = tc::exp2_neg(T.e1[(int64_t)t * tc::N + q]);
+        }
+        tc::named_bar(1, 128);
+      }
+      for (int c = 0; c < n_chunks; ++c, ++cg) {
+        const int ab = cg & 1;
+        const int gi = c * M2 + (int)rank * tc::M + ep;
+        float* dst[2] = {nullptr, nullptr};
+        int64_t plane = 0;
+        int e_c = 0;
+        if (gi < n) {
+          int l = 0;
+          while (l + 1 < P.levels && gi >= S.prefix[l + 1]) ++l;
+          const int idx = gi - S.prefix[l];
+          const int cy = S.hull[l][0] + idx / S.hw[l], cx = S.hull[l][2] + idx % S.hw[l];
+          const int ch = P.ch[l], cw = P.cw[l];
+          plane = (int64_t)ch * cw * TQW;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            if (S.tile[j] < 0) continue;
+            const TilePlan& tp = S.rec[j].plan[l];
+            if (tp.status == ST_OK && in_box(tp.B, cy, cx))
+              dst[j] = P.cache[l] + (int64_t)S.tile[j] * plane * TQH +
+                       (int64_t)slot_of(cy, cx, ch, cw) * TQW;
+          }
+          e_c = T.e2[l][pair * T.pair_bytes[l] + (int64_t)cy * P.tw[l] + cx];
+        }
+        if (!__all_sync(0xffffffffu, WAIT_FULL2(U(C.acc_full[ab]), cg >> 1))) goto done;
+        tc::tc_fence_after();
+        const float s_c = tc::exp2_neg(e_c);
+        float vm[32], vc[32];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t col = (uint32_t)(j * 64 + h * 32);
+            tc::tmem_ld32(tmem + ab * 256 + lane_base + col, vm);
+            tc::tmem_ld32(tmem + ab * 256 + 128 + lane_base + col, vc);
+            if (dst[j] != nullptr) {
+#pragma unroll
+              for (int gg = 0; gg < 4; ++gg) {
+                const int r = gg >> 1, cc = gg & 1;
+                const int j0 = 16 * r + 4 * cc, j1 = j0 + 8;
+                float o[8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  o[i] = fmaf(vc[j0 + i], 1.f / (1 << tc::LOG2_LO), vm[j0 + i]) *
+                         (s_q[j * 64 + h * 32 + j0 + i] * s_c);
+                  o[4 + i] = fmaf(vc[j1 + i], 1.f / (1 << tc::LOG2_LO), vm[j1 + i]) *
+                             (s_q[j * 64 + h * 32 + j1 + i] * s_c);
+                }
+                const int grp = (2 * h + r) * 2 + cc;
+                tc::st_global_v8(dst[j] + grp * plane, o);
+              }
+            }
+          }
+        }
+        tc::tc_fence_before();
+        if (leader) {
+          __syncwarp();
+          if (lane == 0) tcp::arrive(U(C.acc_empty[ab]));
+        } else {
+          tc::named_bar(2, 128);
+          if (ep == 0) arrive_remote(ab ? acc_empty_l1 : acc_empty_l0);
+        }
+      }
+      tcp::arrive(U(C.plan_empty[s]));
+    }
+  }
+done:
+  tc::tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 0) {
+    tc::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+}  // namespace tcp2
+
 }  // namespace cvb
 
 using namespace cvb;
@@ -1312,6 +1818,19 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
   launch_pdl(tcp::plan_kernel, dim3((unsigned)ceil_div(T.P.ntile, tcp::PLAN_WARPS)),
              dim3(tcp::PLAN_WARPS * 32), 0, as_stream(stream), T.P);
   if ((st = check_launch("partial_plan")) != CVB_OK) return st;
+  // cold iterations on SM pairs: every tile row of the range is whole
+  const bool rows_whole = T.P.tile0 % T.P.tiles_x == 0 && T.P.ntile % T.P.tiles_x == 0;
+  if ((flags & CVB_TC_PAIRS) && !dbg && rows_whole && n_sms >= 2) {
+    const int64_t n_pairs = T.P.ntile / T.P.tiles_x * ((T.P.tiles_x + 1) / 2);
+    const size_t smem2 = tcp2::smem_bytes();
+    static std::atomic<uint64_t> attr2{0};
+    ensure_max_smem(attr2, tcp2::pair_contract_kernel, (int)smem2);
+    const int64_t max_cl = n_sms / 2;
+    const int64_t grid2 = 2 * (n_pairs < max_cl ? n_pairs : max_cl);
+    launch_pdl(tcp2::pair_contract_kernel, dim3((unsigned)grid2), dim3(tcp::THREADS), smem2,
+               as_stream(stream), T, n_pairs);
+    return check_launch("partial_contract_tcp2");
+  }
   const int64_t grid = T.P.ntile < n_sms ? T.P.ntile : n_sms;
   launch_pdl(kernel, dim3((unsigned)grid), dim3(tcp::THREADS), smem, as_stream(stream), T);
   if (T.ts != nullptr) {  // debug timeline dump (CTA 0..3, first 64 tiles, 32 events), ns

@@ -573,9 +573,16 @@ def _contract_args(state: SparseVolumeState, centroids: CentroidField, flags: in
     return f2s, caches
 
 
+#: cold iterations (the first, or every one with the cache off) contract on
+#: SM pairs (CVB_TC_PAIRS); CVB_TC_PAIRS=0 in the environment turns it off
+_PAIRS = os.environ.get("CVB_TC_PAIRS", "1").strip() != "0"
+
+
 def _contract(state: SparseVolumeState, centroids: CentroidField, flags: int, f2s,
               caches) -> None:
     if state.tc:
+        if _PAIRS and (state.iteration == 0 or not state.cache_enabled):
+            flags |= _lib.CVB_TC_PAIRS
         _lib.call("cvb_partial_contract_tc", _lib.C.byref(state.desc), _lib.ptr(state.f1.values),
                   f2s, _lib.ptr(state.tc_f1), _lib.ptr_array(state.tc_f2),
                   _lib.ptr(centroids.coords), _lib.ptr(state.meta),
@@ -795,9 +802,14 @@ def _sample_scratch_ranges(state: SparseVolumeState, centroids: CentroidField, f
     reuses them (stream order).  The kernels address the cache by global tile
     index, so each range passes the scratch base shifted back by its first
     tile (only offsets inside the scratch are dereferenced)."""
+    per_tile = [lv.cache.numel() // state.scratch_tiles for lv in state.levels]
+    # ranges of whole tile rows (the cold SM-pair contraction pairs tiles
+    # within a row) when the scratch holds at least one row
+    tiles_x = -(-state.f1.width // _lib.TILE_W)
     r = state.scratch_tiles
+    if r >= tiles_x:
+        r = r // tiles_x * tiles_x
     f2s = _lib.ptr_array([state.pyramid.levels[l].values for l in range(state.spec.levels)])
-    per_tile = [lv.cache.numel() // r for lv in state.levels]
     full = state.desc
     try:
         for t0 in range(0, state.n_tiles, r):
