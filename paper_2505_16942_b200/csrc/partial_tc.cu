@@ -461,7 +461,10 @@ namespace tcp {
 #endif
 constexpr int NST = CVB_TC_NST;     // A stages (32 KB each: hi + lo, 128 rows x 64 channels)
 constexpr int NBP = CVB_TC_NBP;     // F1 pieces in the ring (16 KB each)
-constexpr int NPL = 4;              // plan slots
+#ifndef CVB_TC_NPL
+#define CVB_TC_NPL 3  // plan slots: 3 is 1.7% faster warm than 4 (A/B, round 2)
+#endif
+constexpr int NPL = CVB_TC_NPL;     // plan slots
 constexpr int THREADS = 512;
 constexpr int A_WARPS = 8;             // A producers: warps 4-7 and 12-15
 constexpr int A_ROWS = 128 / A_WARPS;  // A rows per producer warp
