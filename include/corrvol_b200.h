@@ -62,8 +62,6 @@ typedef enum {
                                  box hull per pair) — for cold iterations
                                  (the first after a reset, or CVB_NO_CACHE);
                                  needs a range of whole tile rows, else ignored */
-#define CVB_TC_UNFUSED 128     /* cvb_partial_sample_tc: run the warm contraction
-                                 and the sampler as two kernels (A/B, tests) */
 #define CVB_MAX_LEVELS 8
 
 /* ---- library ------------------------------------------------------------ */
@@ -225,20 +223,6 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
                             const void* const* f2_split_host, const void* coords, int32_t* meta,
                             float* const* cache_levels_host, unsigned long long* counters,
                             int32_t flags, void* stream);
-/* One whole lookup iteration on the tensor-core path (replaces
- * sampled_block_mmm + _gather_patches of sample_iteration, sparse.py:411-452):
- * tiler, incremental contraction and the r=4 sampler writing `out` (the
- * [H,W,L,2r+1,2r+1] cost map, or RAFT's layout with CVB_OUT_RAFT).  Warm
- * iterations (no CVB_TC_PAIRS) with radius 4 and <= 4 levels run as ONE
- * persistent kernel: sampler warps sample each tile from its cache as soon as
- * the tile's new cells are written.  Otherwise (cold iterations with
- * CVB_TC_PAIRS, other radii, CVB_TC_UNFUSED) it is cvb_partial_contract_tc
- * followed by cvb_partial_gather.  Results are bit-identical either way. */
-int cvb_partial_sample_tc(const cvb_partial_desc* desc, const float* f1,
-                          const float* const* f2_levels_host, const void* f1_split,
-                          const void* const* f2_split_host, const void* coords, float scale,
-                          int32_t* meta, float* const* cache_levels_host, float* out,
-                          unsigned long long* counters, int32_t flags, void* stream);
 
 /* Dense all-pairs volume on tcgen05 (the fast dense variant: build_dense_volume
  * / build_volume_pyramid(mode="pool_features"), dense.py:27-45,121-160):

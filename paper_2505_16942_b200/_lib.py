@@ -30,7 +30,6 @@ CVB_PREP_POOL = 8
 CVB_OUT_RAFT = 16
 CVB_ACCESS_NO_TRIM = 32
 CVB_TC_PAIRS = 64
-CVB_TC_UNFUSED = 128
 
 MAX_LEVELS = 8
 TILE_H = 8
@@ -88,9 +87,6 @@ SIGNATURES = {
                                  _i32, _p]),
     "cvb_partial_contract_tc": (C.c_int, [C.POINTER(PartialDesc), _p, C.POINTER(_p), _p,
                                           C.POINTER(_p), _p, _p, C.POINTER(_p), _p, _i32, _p]),
-    "cvb_partial_sample_tc": (C.c_int, [C.POINTER(PartialDesc), _p, C.POINTER(_p), _p,
-                                        C.POINTER(_p), _p, _f32, _p, C.POINTER(_p), _p, _p, _i32,
-                                        _p]),
     "cvb_dense_tc_workspace": (_i64, [C.POINTER(PartialDesc)]),
     "cvb_dense_tc": (C.c_int, [C.POINTER(PartialDesc), _p, C.POINTER(_p), _p, C.POINTER(_p), _p]),
     "cvb_access_union": (C.c_int, [C.POINTER(_p), _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32,

@@ -32,7 +32,6 @@
 #include <stdlib.h>
 #include <string.h>
 
-#include "gather_fast.cuh"
 #include "partial.cuh"
 
 namespace cvb {
@@ -225,7 +224,6 @@ struct TcParams {
   // of every level and the epilogue writes the all-pairs rows
   // dense[l][pixel][cell] instead of cache slots
   float* dense[CVB_MAX_LEVELS];
-  float* out;                          // FUSED instantiation: the cost map the sampler warps write
 };
 
 // Operand preparation, once per image pair.  Every row (a query of F1, a
@@ -478,38 +476,16 @@ constexpr int A_ROWS = 128 / A_WARPS;  // A rows per producer warp
 constexpr unsigned long long WATCHDOG_NS = 20ull * 1000 * 1000 * 1000;
 constexpr int WATCHDOG_CODE = 0x5744;  // 'WD'
 
-// Ring depths and warp roles of the two instantiations.  FUSED (warm
-// iterations): the sampler runs inside the contraction — eight sampler warps
-// (one per query group) sample each tile from its cache as soon as the
-// epilogue has written the tile's new cells, so the samples overlap the next
-// tiles' contraction and the new cells are read back while still in L2.  Its
-// shared memory holds the sampler stages, so the rings are shallower (A 2,
-// F1 pieces 4), the A producers four warps of 32 rows.
-template <bool FUSED>
-struct Cfg {
-  static constexpr int NST = FUSED ? 2 : CVB_TC_NST;
-  static constexpr int NBP = FUSED ? 4 : CVB_TC_NBP;
-  static constexpr int NPL = FUSED ? 4 : CVB_TC_NPL;
-  static constexpr int A_WARPS = FUSED ? 4 : 8;
-  static constexpr int S_WARPS = FUSED ? 8 : 0;  // sampler warps 12..19
-  static constexpr int THREADS = FUSED ? 640 : 512;
-};
-
-template <int NPL_, int NBP_, int NST_>
-struct CtlT {
-  uint64_t plan_full[NPL_], plan_empty[NPL_];
-  uint64_t samp_full[NPL_];  // FUSED: the epilogue has written the slot's tile
-  uint64_t b_full[NBP_], b_empty[NBP_];
-  uint64_t a_full[NST_], a_empty[NST_];
+struct Ctl {
+  uint64_t plan_full[NPL], plan_empty[NPL];
+  uint64_t b_full[NBP], b_empty[NBP];
+  uint64_t a_full[NST], a_empty[NST];
   uint64_t acc_full[2], acc_empty[2];
-  PlanRec slot[NPL_];
+  PlanRec slot[NPL];
   float qscale[tc::N];
   uint32_t tmem;
   int abort;  // watchdog fired in this CTA
 };
-template <bool FUSED>
-using CtlOf = CtlT<Cfg<FUSED>::NPL, Cfg<FUSED>::NBP, Cfg<FUSED>::NST>;
-using Ctl = CtlOf<false>;
 
 __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
   uint32_t ok;
@@ -578,13 +554,9 @@ __device__ __forceinline__ void stamp(const tc::TcParams& T, int64_t it, int e) 
 
 // DEBUG=false is the production instantiation: the CVB_TC_DEBUG knock-outs
 // and the %globaltimer role timeline compile out of it.
-template <bool DEBUG, bool DENSE = false, bool FUSED = false>
-__global__ void __launch_bounds__(Cfg<FUSED>::THREADS, 1)
+template <bool DEBUG, bool DENSE = false>
+__global__ void __launch_bounds__(THREADS, 1)
     partial_contract_tcp_kernel(const __grid_constant__ tc::TcParams T) {
-  constexpr int NST_ = Cfg<FUSED>::NST, NBP_ = Cfg<FUSED>::NBP, NPL_ = Cfg<FUSED>::NPL;
-  constexpr int A_WARPS_ = Cfg<FUSED>::A_WARPS, A_ROWS_ = 128 / A_WARPS_;
-  constexpr int S_WARPS_ = Cfg<FUSED>::S_WARPS;
-  using Ctl_ = CtlOf<FUSED>;
   extern __shared__ uint8_t smem_raw[];
   const PartialParams& P = T.P;
   const int dp = T.dp;
@@ -592,11 +564,9 @@ __global__ void __launch_bounds__(Cfg<FUSED>::THREADS, 1)
   // 1024-byte alignment for the 128B-swizzled A stages
   const uint32_t raw = tc::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-  uint8_t* sA = smem;                        // NST_ x A_STAGE
-  uint8_t* sB = smem + NST_ * tc::A_STAGE;    // NBP_ x B_PIECE
-  // FUSED: the sampler warps' stages, then the control block
-  gfast::WarpStage* s_stage = reinterpret_cast<gfast::WarpStage*>(sB + NBP_ * tc::B_PIECE);
-  Ctl_& C = *reinterpret_cast<Ctl_*>(sB + NBP_ * tc::B_PIECE + S_WARPS_ * sizeof(gfast::WarpStage));
+  uint8_t* sA = smem;                        // NST x A_STAGE
+  uint8_t* sB = smem + NST * tc::A_STAGE;    // NBP x B_PIECE
+  Ctl& C = *reinterpret_cast<Ctl*>(sB + NBP * tc::B_PIECE);
   const uint32_t uB = tc::smem_u32(sB), uA = tc::smem_u32(sA);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   auto U = [](const uint64_t& b) { return tc::smem_u32(&b); };
@@ -608,17 +578,16 @@ __global__ void __launch_bounds__(Cfg<FUSED>::THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (tid == 32) {
-    for (int i = 0; i < NPL_; ++i) {
+    for (int i = 0; i < NPL; ++i) {
       tc::mbar_init(U(C.plan_full[i]), 1);
-      tc::mbar_init(U(C.plan_empty[i]), 1 + 1 + 32 * A_WARPS_ + 128 + 32 * S_WARPS_);
-      tc::mbar_init(U(C.samp_full[i]), 128);
+      tc::mbar_init(U(C.plan_empty[i]), 1 + 1 + 32 * A_WARPS + 128);
     }
-    for (int i = 0; i < NBP_; ++i) {
+    for (int i = 0; i < NBP; ++i) {
       tc::mbar_init(U(C.b_full[i]), 1);
       tc::mbar_init(U(C.b_empty[i]), 1);
     }
-    for (int i = 0; i < NST_; ++i) {
-      tc::mbar_init(U(C.a_full[i]), 32 * A_WARPS_);
+    for (int i = 0; i < NST; ++i) {
+      tc::mbar_init(U(C.a_full[i]), 32 * A_WARPS);
       tc::mbar_init(U(C.a_empty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -640,15 +609,15 @@ __global__ void __launch_bounds__(Cfg<FUSED>::THREADS, 1)
     if (lane == 0) {
       uint32_t pb = 0;  // pieces issued so far
       for (int64_t it = 0;; ++it) {
-        const int s = (int)(it % NPL_);
-        if (!WAIT_FULL(U(C.plan_full[s]), (uint32_t)(it / NPL_))) goto done;
+        const int s = (int)(it % NPL);
+        if (!WAIT_FULL(U(C.plan_full[s]), (uint32_t)(it / NPL))) goto done;
         const int tile_i = C.slot[s].tile;
         if (tile_i < 0) break;
         if (C.slot[s].n_cells > 0) {
           const uint8_t* src = T.f1s + (int64_t)tile_i * n_kb * tc::B_PIECE;
           for (int q = 0; q < n_kb; ++q, ++pb) {
-            const int bs = (int)(pb % NBP_);
-            if (!WAIT_EMPTY(U(C.b_empty[bs]), pb / NBP_)) goto done;
+            const int bs = (int)(pb % NBP);
+            if (!WAIT_EMPTY(U(C.b_empty[bs]), pb / NBP)) goto done;
             stamp<DEBUG>(T, it, 24 + q);
             if (DEBUG && (T.dbg & 8)) {
               arrive(U(C.b_full[bs]));
@@ -671,8 +640,8 @@ __global__ void __launch_bounds__(Cfg<FUSED>::THREADS, 1)
     // the B start by 256 B (+16).
     uint32_t pb = 0, g = 0, cg = 0;
     for (int64_t it = 0;; ++it) {
-      const int s = (int)(it % NPL_);
-      if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.plan_full[s]), (uint32_t)(it / NPL_)))) goto done;
+      const int s = (int)(it % NPL);
+      if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.plan_full[s]), (uint32_t)(it / NPL)))) goto done;
       if (C.slot[s].tile < 0) break;
       if (lane == 0) stamp<DEBUG>(T, it, 1);
       const int n = C.slot[s].n_cells;
@@ -686,13 +655,13 @@ __global__ void __launch_bounds__(Cfg<FUSED>::THREADS, 1)
           const uint32_t d_main = tmem + ab * 128, d_corr = d_main + 64;
           for (int kb = 0; kb < n_kb; ++kb, ++g) {
             const uint32_t pi = pb + kb;
-            const int bs = (int)(pi % NBP_);
+            const int bs = (int)(pi % NBP);
             if (c == 0) {
-              if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.b_full[bs]), pi / NBP_))) goto done;
+              if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.b_full[bs]), pi / NBP))) goto done;
               if (lane == 0) stamp<DEBUG>(T, it, 12 + kb);
             }
-            const int st = (int)(g % NST_);
-            if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.a_full[st]), g / NST_))) goto done;
+            const int st = (int)(g % NST);
+            if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.a_full[st]), g / NST))) goto done;
             tc::tc_fence_after();
             if (c == 0 && lane == 0) stamp<DEBUG>(T, it, 8 + kb);
             const uint32_t a_hi = uA + st * tc::A_STAGE, a_lo = a_hi + tc::A_HALF;
@@ -727,8 +696,8 @@ __global__ void __launch_bounds__(Cfg<FUSED>::THREADS, 1)
     // ---------------- plan loader: one bulk copy per tile record ----------------
     if (lane == 0) {
       for (int64_t it = 0;; ++it) {
-        const int s = (int)(it % NPL_);
-        if (!WAIT_EMPTY(U(C.plan_empty[s]), (uint32_t)(it / NPL_))) goto done;
+        const int s = (int)(it % NPL);
+        if (!WAIT_EMPTY(U(C.plan_empty[s]), (uint32_t)(it / NPL))) goto done;
         const int64_t t = atomicAdd(tile_counter(P), 1);  // dynamic tile scheduler
         if (t >= P.ntile) {  // end of the work list: a sentinel record
           C.slot[s].tile = -1;
@@ -741,21 +710,21 @@ __global__ void __launch_bounds__(Cfg<FUSED>::THREADS, 1)
         stamp<DEBUG>(T, it, 0);
       }
     }
-  } else if ((warp >= 4 && warp < 8) || (!FUSED && warp >= 12)) {
+  } else if ((warp >= 4 && warp < 8) || warp >= 12) {
     // ---------------- A producers: cp.async of the new cells ----------------
-    // warp aw owns A rows A_ROWS_*aw ..+A_ROWS_-1 (eight warps: per-chunk cell
+    // warp aw owns A rows A_ROWS*aw ..+A_ROWS-1 (eight warps: per-chunk cell
     // decoding and issue run in parallel; -3% at iteration 0 against four);
     // per 4-row group one warp instruction
     // moves 4 full 128-byte rows (8 lanes x 16 B each, full L2 lines) into
     // the 128B-swizzled stage; completion is signalled per thread with
     // cp.async.mbarrier.arrive.noinc, so no producer thread ever waits on
     // its own copies.
-    const int aw = warp < 8 ? warp - 4 : warp - 8;  // FUSED: warps 4-7 only
+    const int aw = warp < 8 ? warp - 4 : warp - 8;
     const int sub = lane >> 3, chunk = lane & 7;
     uint32_t g = 0;  // A stages issued
     for (int64_t it = 0;; ++it) {
-      const int s = (int)(it % NPL_);
-      if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.plan_full[s]), (uint32_t)(it / NPL_)))) goto done;
+      const int s = (int)(it % NPL);
+      if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.plan_full[s]), (uint32_t)(it / NPL)))) goto done;
       const PlanRec& S = C.slot[s];
       if (S.tile < 0) break;
       const int n = S.n_cells;
@@ -763,7 +732,7 @@ __global__ void __launch_bounds__(Cfg<FUSED>::THREADS, 1)
       const int64_t pair = P.batch > 1 ? S.tile / P.tiles_pp : 0;
       for (int c = 0; c < n_chunks; ++c) {
         // source row of A row 32aw + lane (hi plane; lo = hi + plane)
-        const int gi = c * tc::M + A_ROWS_ * aw + (lane % A_ROWS_);
+        const int gi = c * tc::M + A_ROWS * aw + (lane % A_ROWS);
         const __half* my_hi = nullptr;
         int64_t my_plane = 0;
         if (gi < n) {
@@ -774,19 +743,19 @@ __global__ void __launch_bounds__(Cfg<FUSED>::THREADS, 1)
           my_plane = T.plane[cr.level];
         }
         for (int kb = 0; kb < n_kb; ++kb, ++g) {
-          const int st = (int)(g % NST_);
-          if (!__all_sync(0xffffffffu, WAIT_EMPTY(U(C.a_empty[st]), g / NST_))) goto done;
+          const int st = (int)(g % NST);
+          if (!__all_sync(0xffffffffu, WAIT_EMPTY(U(C.a_empty[st]), g / NST))) goto done;
           if (c == 0 && tid == 128) stamp<DEBUG>(T, it, 16 + kb);
           if (!(DEBUG && (T.dbg & 1))) {
             const uint32_t stage = uA + st * tc::A_STAGE;
 #pragma unroll
-            for (int i = 0; i < A_ROWS_ / 4; ++i) {
-              const int rl = 4 * i + sub;  // row within the warp's A_ROWS_
+            for (int i = 0; i < A_ROWS / 4; ++i) {
+              const int rl = 4 * i + sub;  // row within the warp's A_ROWS
               const __half* hi = reinterpret_cast<const __half*>(
                   __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_hi), rl));
               const int64_t pl = __shfl_sync(0xffffffffu, my_plane, rl);
               if (hi != nullptr) {
-                const int row = A_ROWS_ * aw + rl;
+                const int row = A_ROWS * aw + rl;
                 const uint32_t dst = stage + row * 128 + ((chunk ^ (row & 7)) << 4);
                 const __half* src = hi + kb * tc::KP + chunk * 8;
                 tc::cp_async16(dst, src);
@@ -811,8 +780,8 @@ __global__ void __launch_bounds__(Cfg<FUSED>::THREADS, 1)
     float* s_q = reinterpret_cast<float*>(&C.qscale[0]);
     uint32_t cg = 0;
     for (int64_t it = 0;; ++it) {
-      const int s = (int)(it % NPL_);
-      if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.plan_full[s]), (uint32_t)(it / NPL_)))) goto done;
+      const int s = (int)(it % NPL);
+      if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.plan_full[s]), (uint32_t)(it / NPL)))) goto done;
       const PlanRec& S = C.slot[s];
       if (S.tile < 0) break;
       const int64_t tile = S.tile;
@@ -895,26 +864,6 @@ __global__ void __launch_bounds__(Cfg<FUSED>::THREADS, 1)
         arrive(U(C.acc_empty[ab]));
       }
       if (tid == 256) stamp<DEBUG>(T, it, 4);
-      if (FUSED) arrive(U(C.samp_full[s]));  // release: the tile's cache stores
-      arrive(U(C.plan_empty[s]));
-    }
-  } else if (FUSED && warp >= 12 && warp < 12 + S_WARPS_) {
-    // ---------------- sampler (FUSED): query group warp-12 of each tile ----------------
-    // waits until the epilogue has written the tile's new cells (acquire),
-    // then samples the group at every level straight from the tile cache
-    // (gather_fast.cuh; coherent loads: some cells were written by this CTA
-    // moments ago and are still in L2)
-    const int grp = warp - 12;
-    const int li = lane >> 3;
-    for (int64_t it = 0;; ++it) {
-      const int s = (int)(it % NPL_);
-      if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.plan_full[s]), (uint32_t)(it / NPL_)))) goto done;
-      const PlanRec& S = C.slot[s];
-      if (S.tile < 0) break;
-      if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.samp_full[s]), (uint32_t)(it / NPL_)))) goto done;
-      const int status = li < P.levels ? S.plan[li].status : ST_EMPTY;
-      if (!(DEBUG && (T.dbg & 32)))
-        gfast::sample_group<false>(P, S.tile, grp, status, T.out, 0, P.levels, s_stage[grp], lane);
       arrive(U(C.plan_empty[s]));
     }
   }
@@ -1086,11 +1035,8 @@ __global__ void dense_plan_kernel(PartialParams P) {
   for (int i = 0; i < PLAN_INTS; ++i) rec[i] = src[i];
 }
 
-template <bool FUSED = false>
 size_t smem_bytes() {
-  using K = Cfg<FUSED>;
-  return (size_t)K::NST * tc::A_STAGE + (size_t)K::NBP * tc::B_PIECE +
-         (size_t)K::S_WARPS * sizeof(gfast::WarpStage) + sizeof(CtlOf<FUSED>) + 1024;
+  return (size_t)NST * tc::A_STAGE + (size_t)NBP * tc::B_PIECE + sizeof(Ctl) + 1024;
 }
 
 // SM count per device (the persistent grid size), queried once per device.
@@ -1816,16 +1762,14 @@ int cvb_dense_tc(const cvb_partial_desc* desc, const void* f1_split,
   return check_launch("dense_tc");
 }
 
-// Parameters of one tensor-core iteration (shared by the contraction-only and
-// the contract+sample entry points); 1 when there is nothing to launch.
-static int tc_params(const cvb_partial_desc* desc, const float* f1,
-                     const float* const* f2_levels_host, const void* f1_split,
-                     const void* const* f2_split_host, const void* coords, float scale,
-                     int32_t* meta, float* const* cache_levels_host,
-                     unsigned long long* counters, int32_t flags, void* stream,
-                     tc::TcParams& T) {
+int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
+                            const float* const* f2_levels_host, const void* f1_split,
+                            const void* const* f2_split_host, const void* coords, int32_t* meta,
+                            float* const* cache_levels_host, unsigned long long* counters,
+                            int32_t flags, void* stream) {
+  tc::TcParams T;
   memset(&T, 0, sizeof(T));
-  int st = cvb_internal_build_params(desc, f1, f2_levels_host, coords, scale, meta,
+  int st = cvb_internal_build_params(desc, f1, f2_levels_host, coords, 1.0f, meta,
                                      cache_levels_host, counters, flags, T.P);
   if (st != CVB_OK) return st;
   CVB_REQUIRE(!(flags & CVB_STRICT), "tensor-core contraction has no strict mode");
@@ -1853,25 +1797,15 @@ static int tc_params(const cvb_partial_desc* desc, const float* f1,
     return CVB_ERR_CUDA;
   }
   T.watchdog = word != nullptr ? tcp::watchdog_dev : nullptr;
-  return T.P.ntile == 0 ? 1 : CVB_OK;
-}
-
-static int tc_debug_flags() {
+  if (T.P.ntile == 0) return CVB_OK;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int n_sms = tcp::sm_count(dev);
   static int dbg = -1;  // CVB_TC_DEBUG: profiling knock-outs / timeline (debug kernel)
   if (dbg < 0) {
     const char* e = getenv("CVB_TC_DEBUG");
     dbg = e ? atoi(e) : 0;
   }
-  return dbg;
-}
-
-// tiler + contraction (single-tile kernel, SM pairs for cold iterations)
-static int tc_contract(tc::TcParams& T, int32_t flags, void* stream) {
-  int st;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const int n_sms = tcp::sm_count(dev);
-  const int dbg = tc_debug_flags();
   T.dbg = dbg;
   static unsigned long long* ts_buf = nullptr;
   T.ts = nullptr;
@@ -1918,54 +1852,6 @@ static int tc_contract(tc::TcParams& T, int32_t flags, void* stream) {
     }
   }
   return check_launch("partial_contract_tcp");
-}
-
-int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
-                            const float* const* f2_levels_host, const void* f1_split,
-                            const void* const* f2_split_host, const void* coords, int32_t* meta,
-                            float* const* cache_levels_host, unsigned long long* counters,
-                            int32_t flags, void* stream) {
-  tc::TcParams T;
-  const int st = tc_params(desc, f1, f2_levels_host, f1_split, f2_split_host, coords, 1.0f, meta,
-                           cache_levels_host, counters, flags, stream, T);
-  if (st != CVB_OK) return st == 1 ? CVB_OK : st;
-  return tc_contract(T, flags, stream);
-}
-
-int cvb_partial_sample_tc(const cvb_partial_desc* desc, const float* f1,
-                          const float* const* f2_levels_host, const void* f1_split,
-                          const void* const* f2_split_host, const void* coords, float scale,
-                          int32_t* meta, float* const* cache_levels_host, float* out,
-                          unsigned long long* counters, int32_t flags, void* stream) {
-  tc::TcParams T;
-  int st = tc_params(desc, f1, f2_levels_host, f1_split, f2_split_host, coords, scale, meta,
-                     cache_levels_host, counters, flags, stream, T);
-  if (st != CVB_OK) return st == 1 ? CVB_OK : st;
-  CVB_REQUIRE(out, "partial_sample_tc: null output");
-  const int dbg = tc_debug_flags();
-  const bool fused = !(flags & (CVB_TC_PAIRS | CVB_TC_UNFUSED)) && T.P.radius == 4 &&
-                     T.P.levels <= gfast::MAXL && (dbg == 0 || (dbg & 128));
-  if (!fused) {
-    if ((st = tc_contract(T, flags, stream)) != CVB_OK) return st;
-    return launch_gather_kernel(T.P, out, false, as_stream(stream));
-  }
-  T.out = out;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const int n_sms = tcp::sm_count(dev);
-  const size_t smem = tcp::smem_bytes<true>();
-  T.dbg = dbg;  // CVB_TC_DEBUG with bit 128: the fused kernel's debug instantiation
-  auto kernel = dbg ? tcp::partial_contract_tcp_kernel<true, false, true>
-                    : tcp::partial_contract_tcp_kernel<false, false, true>;
-  static std::atomic<uint64_t> attr{0}, attr_dbg{0};
-  ensure_max_smem(dbg ? attr_dbg : attr, kernel, (int)smem);
-  launch_pdl(tcp::plan_kernel, dim3((unsigned)ceil_div(T.P.ntile, tcp::PLAN_WARPS)),
-             dim3(tcp::PLAN_WARPS * 32), 0, as_stream(stream), T.P);
-  if ((st = check_launch("partial_plan")) != CVB_OK) return st;
-  const int64_t grid = T.P.ntile < n_sms ? T.P.ntile : n_sms;
-  launch_pdl(kernel, dim3((unsigned)grid), dim3(tcp::Cfg<true>::THREADS), smem, as_stream(stream),
-             T);
-  return check_launch("partial_sample_tcp");
 }
 
 }  // extern "C"

@@ -494,7 +494,7 @@ def _setup_tile(state: SparseVolumeState, tile_caps, hard_limit_bytes: Optional[
         # overlap contraction and gathering across tile ranges: measured on
         # B200 at C4, no gain (the contraction's shared memory keeps the
         # sampler from co-residing), so off by default
-        state.pipeline_splits = max(1, int(pipeline_splits or _ENV_SPLITS or 1))
+        state.pipeline_splits = max(1, int(pipeline_splits or 1))
 
 
 @on_device
@@ -576,13 +576,6 @@ def _contract_args(state: SparseVolumeState, centroids: CentroidField, flags: in
 #: cold iterations (the first, or every one with the cache off) contract on
 #: SM pairs (CVB_TC_PAIRS); CVB_TC_PAIRS=0 in the environment turns it off
 _PAIRS = os.environ.get("CVB_TC_PAIRS", "1").strip() != "0"
-#: experiment knobs: tile ranges per iteration, and whether range i's sampler
-#: follows its contraction on the same stream (serial) or a side stream
-#: warm iterations as one fused contraction + sampler kernel; CVB_FUSED=0
-#: runs them as two kernels (A/B measurements, equality tests)
-_FUSED = os.environ.get("CVB_FUSED", "1").strip() != "0"
-_ENV_SPLITS = int(os.environ.get("CVB_PIPELINE_SPLITS", "0") or 0)
-_SPLIT_SERIAL = os.environ.get("CVB_SPLIT_MODE", "serial") == "serial"
 
 
 def _contract(state: SparseVolumeState, centroids: CentroidField, flags: int, f2s,
@@ -852,32 +845,9 @@ def _sample_tile_mode(state: SparseVolumeState, centroids: CentroidField,
         return
     f2s, caches = _contract_args(state, centroids, flags)
     splits = state.pipeline_splits
-    if splits <= 1 and state.tc:
-        # one entry per iteration: warm iterations run contraction + sampler
-        # as one persistent kernel (cold ones: SM-pair contraction, sampler)
-        if _PAIRS and (state.iteration == 0 or not state.cache_enabled):
-            flags |= _lib.CVB_TC_PAIRS
-        if not _FUSED:
-            flags |= _lib.CVB_TC_UNFUSED
-        _lib.call("cvb_partial_sample_tc", _lib.C.byref(state.desc), _lib.ptr(state.f1.values),
-                  f2s, _lib.ptr(state.tc_f1), _lib.ptr_array(state.tc_f2),
-                  _lib.ptr(centroids.coords), state.spec.scale(state.f1.dims),
-                  _lib.ptr(state.meta), caches, _lib.ptr(out), _lib.ptr(state._dev_counters),
-                  flags, stream_handle())
-        return
     if splits <= 1:
         _contract(state, centroids, flags, f2s, caches)
         _gather(state, centroids, flags, f2s, caches, out)
-        return
-    if _SPLIT_SERIAL:
-        full = state.desc
-        try:
-            for d in _range_descs(state, splits):
-                state.desc = d
-                _contract(state, centroids, flags, f2s, caches)
-                _gather(state, centroids, flags, f2s, caches, out)
-        finally:
-            state.desc = full
         return
     main = torch.cuda.current_stream(state.device)
     if state._side_stream is None:
