@@ -6,14 +6,15 @@
 //   * D[128 cells x 64 queries] = A[cells x K] . B[queries x K]^T with
 //     M=128, N=64, K=16 `tcgen05.mma.cta_group::1.kind::f16`, accumulators in
 //     TMEM (a 2-deep ring of main + corr accumulators, 64 fp32 columns each);
-//   * split precision: every fp32 value x (pre-scaled by a per-tensor power of
+//   * split precision: every fp32 value x (pre-scaled by a per-row power of
 //     two so it sits in fp16 range) is stored as hi = fp16(x) and
-//     lo = fp16((x - hi) * 2^11); x*y = hi_x*hi_y + 2^-11 (hi_x*lo_y + lo_x*hi_y)
-//     + O(2^-22).  Per K-step one N=128 MMA (the F1 piece's hi and lo rows
-//     form one 128-row B matrix: main += hi.hi and corr += hi.lo, reading
-//     A_hi from shared memory once) and one N=64 MMA (corr += lo.hi) keep ~22
+//     lo = fp16(x - hi); x*y = hi_x*hi_y + hi_x*lo_y + lo_x*hi_y + O(2^-22).
+//     Per K-step one N=128 MMA (the F1 piece's hi and lo rows form one
+//     128-row B matrix: main += hi.hi and corr += hi.lo, reading A_hi from
+//     shared memory once) and one N=64 MMA (corr += lo.hi) keep ~22
 //     significant bits per product (products of two fp16 are exact in the
-//     fp32 accumulator);
+//     fp32 accumulator; the SM-pair kernel sums all three into one
+//     accumulator);
 //   * operands are pre-split once per image pair (cvb_tc_prepare): the F1
 //     tile is a contiguous image of its shared-memory layout cut into K
 //     pieces of 64 channels (16 KB: hi 8 KB + lo 8 KB), each fetched with one
@@ -23,7 +24,7 @@
 //     128 per chunk) stream by cp.async (8 lanes per 128-byte row) through a
 //     4-stage ring of 128B-swizzled K=64 stages (32 KB: hi + lo) that never
 //     drains between tiles;
-//   * the epilogue reads TMEM with tcgen05.ld, combines main + 2^-11 corr,
+//   * the epilogue reads TMEM with tcgen05.ld, combines main + corr,
 //     removes the power-of-two scales and writes each cell's 64 query costs
 //     into its cache slot.
 #include <cuda_fp16.h>
@@ -45,7 +46,8 @@ constexpr int A_STAGE = 2 * A_HALF;      // 32 KB
 constexpr int B_HALF = N * KP * 2;       // 8 KB (hi or lo)
 constexpr int B_PIECE = 2 * B_HALF;      // 16 KB
 constexpr int MAX_DP = 256;
-constexpr int LOG2_LO = 11;              // lo part scale
+// lo = fp16(x - hi), unscaled: the hi.lo and lo.hi products have the scale
+// of hi.hi, so they may share its accumulator (the SM-pair kernel does)
 constexpr int TARGET_EXP = 14;           // max |x * 2^e| < 2^14
 
 // instruction descriptor: D f32, A/B f16, both K-major, N=64, M=128
@@ -202,7 +204,7 @@ __device__ __forceinline__ void split8(const float (&x)[8], float s, uint4& hi, 
   for (int i = 0; i < 8; ++i) {
     const float v = x[i] * s;
     h[i] = __float2half_rn(v);
-    l[i] = __float2half_rn((v - __half2float(h[i])) * (float)(1 << LOG2_LO));
+    l[i] = __float2half_rn(v - __half2float(h[i]));
   }
   hi = *reinterpret_cast<uint4*>(h);
   lo = *reinterpret_cast<uint4*>(l);
@@ -449,7 +451,7 @@ __device__ __forceinline__ CellRef cell_of(int g, const TilePlan* plans, const i
 //                into a 128B-swizzled NST-stage ring, completion tracked by
 //                cp.async.mbarrier.arrive.noinc
 //   warps 8-11   epilogue: tcgen05.ld of a 2-deep TMEM accumulator ring,
-//                main + 2^-11 corr, cache-slot stores
+//                main + corr, cache-slot stores
 // ---------------------------------------------------------------------------
 namespace tcp {
 
@@ -482,7 +484,7 @@ struct Ctl {
   uint64_t a_full[NST], a_empty[NST];
   uint64_t acc_full[2], acc_empty[2];
   PlanRec slot[NPL];
-  float qscale[tc::N];
+  alignas(16) int8_t e1[NPL][tc::N];  // the slot's tile's query exponents (bulk-copied with the plan)
   uint32_t tmem;
   int abort;  // watchdog fired in this CTA
 };
@@ -674,6 +676,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int k = 0; k < tc::KP / 16; ++k) {
                   const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
                   // cols 0-63 += A_hi B_hi (main), cols 64-127 += A_hi B_lo (corr)
+                  // (three N=64 MMAs into one accumulator, halving the epilogue's
+                  // TMEM reads, measured 3% slower per step: A_hi read twice)
                   tc::mma_f16<tc::IDESC_N128>(d_main, dah + 2 * k, dbh + 16 * k, acc);
                   tc::mma_f16(d_corr, dal + 2 * k, dbh + 16 * k, 1u);  // corr += A_lo B_hi
                 }
@@ -704,9 +708,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           arrive(U(C.plan_full[s]));
           break;
         }
-        tc::mbar_expect_tx(U(C.plan_full[s]), (uint32_t)sizeof(PlanRec));
+        // the plan record and the tile's 64 query exponents (the epilogue's
+        // scales: no global load on its per-tile path)
+        tc::mbar_expect_tx(U(C.plan_full[s]), (uint32_t)sizeof(PlanRec) + tc::N);
         tc::bulk_g2s(tc::smem_u32(&C.slot[s]), P.plans + (P.tile0 + t) * PLAN_INTS,
                      (uint32_t)sizeof(PlanRec), U(C.plan_full[s]));
+        tc::bulk_g2s(tc::smem_u32(&C.e1[s][0]), T.e1 + (P.tile0 + t) * tc::N, tc::N,
+                     U(C.plan_full[s]));
         stamp<DEBUG>(T, it, 0);
       }
     }
@@ -777,7 +785,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------- epilogue (128 threads = TMEM lanes) ----------------
     const int ep = tid - 256;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    float* s_q = reinterpret_cast<float*>(&C.qscale[0]);
     uint32_t cg = 0;
     for (int64_t it = 0;; ++it) {
       const int s = (int)(it % NPL);
@@ -789,12 +796,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int n_chunks = (n + tc::M - 1) / tc::M;
       const int64_t pair = P.batch > 1 ? tile / P.tiles_pp : 0;
       const TileRef tr = DENSE ? tile_ref(P, tile) : TileRef{0, 0, 0, 0};
-      if (n_chunks > 0) {
-        // the tile's 64 query scales 2^-e_q
-        tc::named_bar(1, 128);
-        if (ep < tc::N) s_q[ep] = tc::exp2_neg(T.e1[tile * tc::N + ep]);
-        tc::named_bar(1, 128);
-      }
+      const int8_t* e_q = C.e1[s];  // query exponents: scale 2^-(e_q + e_c), exact
       for (int c = 0; c < n_chunks; ++c, ++cg) {
         const int ab = cg & 1;
         // the row's cell, cache slot and exponent depend only on the plan:
@@ -820,7 +822,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.acc_full[ab]), cg >> 1))) goto done;
         tc::tc_fence_after();
         if (c == 0 && tid == 256) stamp<DEBUG>(T, it, 20);
-        const float s_c = tc::exp2_neg(e_c);
         float vm[32], vc[32];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -837,11 +838,9 @@ __global__ void __launch_bounds__(THREADS, 1)
               float o[8];
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
-                // (main + 2^-11 corr) * 2^-(e_q + e_c): exact power-of-two scales
-                o[i] = fmaf(vc[j0 + i], 1.f / (1 << tc::LOG2_LO), vm[j0 + i]) *
-                       (s_q[h * 32 + j0 + i] * s_c);
-                o[4 + i] = fmaf(vc[j1 + i], 1.f / (1 << tc::LOG2_LO), vm[j1 + i]) *
-                           (s_q[h * 32 + j1 + i] * s_c);
+                // (main + corr) * 2^-(e_q + e_c): exact power-of-two scales
+                o[i] = (vm[j0 + i] + vc[j0 + i]) * tc::exp2_neg(e_q[h * 32 + j0 + i] + e_c);
+                o[4 + i] = (vm[j1 + i] + vc[j1 + i]) * tc::exp2_neg(e_q[h * 32 + j1 + i] + e_c);
               }
               const int g = (2 * h + r) * 2 + c;  // == qgroup(4h + 2r, 4c)
               tc::st_global_v8(dst + g * plane, o);
@@ -855,7 +854,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               const int py = tr.ty * TQH + (q >> 3), px = tr.tx * TQW + (q & 7);
               if (py < P.h1 && px < P.w1)
                 dd[((int64_t)py * P.w1 + px) * plane] =
-                    fmaf(vc[j], 1.f / (1 << tc::LOG2_LO), vm[j]) * (s_q[q] * s_c);
+                    (vm[j] + vc[j]) * tc::exp2_neg(e_q[q] + e_c);
             }
           }
         }
@@ -1102,9 +1101,12 @@ int* watchdog_word(cudaStream_t s) {
 // hull of their two boxes once, as M=256 chunks: each CTA gathers half of
 // every chunk's cell rows (A) and holds its own tile's F1 image (B = the two
 // tiles' 128 queries, N-split across the CTAs); the leader CTA issues
-// tcgen05.mma.cta_group::2 (main = A_hi.B_hi, corr = A_hi.B_lo + A_lo.B_hi,
-// three N=128 MMAs per K=16 step) and every commit is multicast to both
-// CTAs' barriers.  Each CTA's TMEM holds its 128 cells x 128 queries; its
+// tcgen05.mma.cta_group::2 (A_hi.B_hi + A_hi.B_lo + A_lo.B_hi, three N=128
+// MMAs per K=16 step into ONE accumulator: lo is unscaled, so the products
+// share a scale and the epilogue reads 128 TMEM columns per chunk instead of
+// 256 — TMEM reads, ~64 B/clk/SM, paced the epilogue) and every commit is
+// multicast to both CTAs' barriers.  Each CTA's TMEM holds its 128 cells x
+// 128 queries in a 4-deep accumulator ring; its
 // epilogue writes every cell that lies in tile j's box into tile j's cache
 // (the same cells the single-tile kernel writes when the tile is cold; a
 // cell of the previous box is rewritten with its own value when it is not).
@@ -1122,6 +1124,9 @@ using tcp::A_WARPS;
 using tcp::A_ROWS;
 
 constexpr int M2 = 256;  // cells per pair chunk (128 per CTA)
+// one fp32 accumulator per chunk (hi.hi + hi.lo + lo.hi share a scale: lo
+// is unscaled): 128 TMEM columns per buffer, a 4-deep ring in 512 columns
+constexpr int NACC = 4;
 constexpr int RELAY_LANES = NST + 1;  // follower relay: one lane per A stage + one for B
 
 __device__ __forceinline__ uint32_t cta_rank() {
@@ -1187,9 +1192,9 @@ struct Ctl2 {
   unsigned long long pidx[NPL];    // follower: pair index mailbox (written by the leader)
   uint64_t b_full[NBP], b_empty[NBP];
   uint64_t a_full[NST], a_empty[NST];
-  uint64_t acc_full[2], acc_empty[2];
+  uint64_t acc_full[NACC], acc_empty[NACC];
   PairSlot slot[NPL];
-  float qscale[2 * tc::N];
+  alignas(16) int8_t e1[NPL][2][tc::N];  // both tiles' query exponents (bulk-copied with the plans)
   uint32_t tmem;
   int abort;
 };
@@ -1217,6 +1222,9 @@ __device__ __forceinline__ void pair_tiles(const PartialParams& P, int64_t pidx,
 #define WAIT_FULL_CL(bar, k) tcp::wait_phase((bar), (uint32_t)(k) & 1u, &C.abort, T.watchdog)
 #define WAIT_EMPTY_CL(bar, k) tcp::wait_phase((bar), ((uint32_t)(k) & 1u) ^ 1u, &C.abort, T.watchdog)
 
+// DEBUG=true: the CVB_TC_DEBUG knock-outs (1 A loads, 2 epilogue stores, 4 MMAs,
+// 8 F1 loads) for profiling; DEBUG=false is the production instantiation.
+template <bool DEBUG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     pair_contract_kernel(const __grid_constant__ tc::TcParams T, int64_t n_pairs) {
   extern __shared__ uint8_t smem_raw[];
@@ -1257,7 +1265,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       tc::mbar_init(U(C.a_full[i]), 32 * A_WARPS + (leader ? 1 : 0));
       tc::mbar_init(U(C.a_empty[i]), 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NACC; ++i) {
       tc::mbar_init(U(C.acc_full[i]), 1);
       tc::mbar_init(U(C.acc_empty[i]), 4 + 1);  // leader: 4 local epilogue warps + the follower
     }
@@ -1287,6 +1295,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           for (int q = 0; q < n_kb; ++q, ++pb) {
             const int bs = (int)(pb % NBP);
             if (!WAIT_EMPTY2(U(C.b_empty[bs]), pb / NBP)) goto done;
+            if (DEBUG && (T.dbg & 8)) {
+              tcp::arrive(U(C.b_full[bs]));
+              continue;
+            }
             tc::mbar_expect_tx(U(C.b_full[bs]), tc::B_PIECE);
             tc::bulk_g2s(uB + bs * tc::B_PIECE, src + (int64_t)q * tc::B_PIECE, tc::B_PIECE,
                          U(C.b_full[bs]));
@@ -1308,10 +1320,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (n > 0) {
           const int n_chunks = (n + M2 - 1) / M2;
           for (int c = 0; c < n_chunks; ++c, ++cg) {
-            const int ab = cg & 1;
-            if (!__all_sync(0xffffffffu, WAIT_EMPTY_CL(U(C.acc_empty[ab]), cg >> 1))) goto done;
+            const int ab = (int)(cg % NACC);
+            if (!__all_sync(0xffffffffu, WAIT_EMPTY_CL(U(C.acc_empty[ab]), cg / NACC))) goto done;
             tc::tc_fence_after();
-            const uint32_t d_main = tmem + ab * 256, d_corr = d_main + 128;
+            const uint32_t d_acc = tmem + ab * 128;
             for (int kb = 0; kb < n_kb; ++kb, ++g) {
               const uint32_t pi = pb + kb;
               const int bs = (int)(pi % NBP);
@@ -1328,10 +1340,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               if (tc::elect_one()) {
 #pragma unroll
                 for (int k = 0; k < tc::KP / 16; ++k) {
+                  if (DEBUG && (T.dbg & 4)) break;
                   const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-                  mma2<IDESC2>(d_main, dah + 2 * k, dbh + 16 * k, acc);  // A_hi B_hi
-                  mma2<IDESC2>(d_corr, dah + 2 * k, dbl + 16 * k, acc);  // A_hi B_lo
-                  mma2<IDESC2>(d_corr, dal + 2 * k, dbh + 16 * k, 1u);   // A_lo B_hi
+                  mma2<IDESC2>(d_acc, dah + 2 * k, dbh + 16 * k, acc);  // A_hi B_hi
+                  mma2<IDESC2>(d_acc, dah + 2 * k, dbl + 16 * k, 1u);   // A_hi B_lo
+                  mma2<IDESC2>(d_acc, dal + 2 * k, dbh + 16 * k, 1u);   // A_lo B_hi
                 }
                 commit_mc(U(C.a_empty[st]));
                 if (c == n_chunks - 1) commit_mc(U(C.b_empty[bs]));
@@ -1409,12 +1422,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         S.tile[0] = t0;
         S.tile[1] = t1;
         const uint32_t rec_bytes = (uint32_t)sizeof(PlanRec);
-        tc::mbar_expect_tx(U(C.plan_copy[s]), rec_bytes * (t1 >= 0 ? 2 : 1));
+        tc::mbar_expect_tx(U(C.plan_copy[s]), (rec_bytes + tc::N) * (t1 >= 0 ? 2 : 1));
         tc::bulk_g2s(tc::smem_u32(&S.rec[0]), P.plans + (int64_t)t0 * PLAN_INTS, rec_bytes,
                      U(C.plan_copy[s]));
-        if (t1 >= 0)
+        tc::bulk_g2s(tc::smem_u32(&C.e1[s][0][0]), T.e1 + (int64_t)t0 * tc::N, tc::N,
+                     U(C.plan_copy[s]));
+        if (t1 >= 0) {
           tc::bulk_g2s(tc::smem_u32(&S.rec[1]), P.plans + (int64_t)t1 * PLAN_INTS, rec_bytes,
                        U(C.plan_copy[s]));
+          tc::bulk_g2s(tc::smem_u32(&C.e1[s][1][0]), T.e1 + (int64_t)t1 * tc::N, tc::N,
+                       U(C.plan_copy[s]));
+        }
         if (!WAIT_FULL2(U(C.plan_copy[s]), (uint32_t)(it / NPL))) goto done;
         int acc = 0;
         for (int l = 0; l < CVB_MAX_LEVELS; ++l) {
@@ -1475,6 +1493,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const int st = (int)(g % NST);
           if (!__all_sync(0xffffffffu, WAIT_EMPTY2(U(C.a_empty[st]), g / NST))) goto done;
           const uint32_t stage = uA + st * tc::A_STAGE;
+          if (DEBUG && (T.dbg & 1)) {
+            tcp::arrive(U(C.a_full[st]));
+            continue;
+          }
 #pragma unroll
           for (int i = 0; i < A_ROWS / 4; ++i) {
             const int rl = 4 * i + sub;
@@ -1500,8 +1522,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     // ---------------- epilogue: this CTA's 128 cells x both tiles' queries ----------------
     const int ep = tid - 256;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    float* s_q = &C.qscale[0];
-    const uint32_t acc_empty_l0 = mapa(U(C.acc_empty[0]), 0), acc_empty_l1 = mapa(U(C.acc_empty[1]), 0);
+    const uint32_t acc_empty_base = mapa(U(C.acc_empty[0]), 0);  // leader's ring (remote)
     uint32_t cg = 0;
     for (int64_t it = 0;; ++it) {
       const int s = (int)(it % NPL);
@@ -1511,17 +1532,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const int n = S.n_cells;
       const int n_chunks = (n + M2 - 1) / M2;
       const int64_t pair = P.batch > 1 ? S.tile[0] / P.tiles_pp : 0;
-      if (n_chunks > 0) {
-        tc::named_bar(1, 128);
-        {
-          const int j = ep >> 6, q = ep & 63;
-          const int t = S.tile[j] >= 0 ? S.tile[j] : S.tile[0];
-          s_q[ep] = tc::exp2_neg(T.e1[(int64_t)t * tc::N + q]);
-        }
-        tc::named_bar(1, 128);
-      }
+      // both tiles' query exponents: scale 2^-(e_q + e_c), exact
+      const int8_t(&e_q)[2][tc::N] = C.e1[s];
       for (int c = 0; c < n_chunks; ++c, ++cg) {
-        const int ab = cg & 1;
+        const int ab = (int)(cg % NACC);
         const int gi = c * M2 + (int)rank * tc::M + ep;
         float* dst[2] = {nullptr, nullptr};
         int64_t plane = 0;
@@ -1543,18 +1557,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           }
           e_c = T.e2[l][pair * T.pair_bytes[l] + (int64_t)cy * P.tw[l] + cx];
         }
-        if (!__all_sync(0xffffffffu, WAIT_FULL2(U(C.acc_full[ab]), cg >> 1))) goto done;
+        if (!__all_sync(0xffffffffu, WAIT_FULL2(U(C.acc_full[ab]), cg / NACC))) goto done;
         tc::tc_fence_after();
-        const float s_c = tc::exp2_neg(e_c);
-        float vm[32], vc[32];
+        float vm[32];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const uint32_t col = (uint32_t)(j * 64 + h * 32);
-            tc::tmem_ld32(tmem + ab * 256 + lane_base + col, vm);
-            tc::tmem_ld32(tmem + ab * 256 + 128 + lane_base + col, vc);
-            if (dst[j] != nullptr) {
+            tc::tmem_ld32(tmem + ab * 128 + lane_base + col, vm);
+            if (dst[j] != nullptr && !(DEBUG && (T.dbg & 2))) {
 #pragma unroll
               for (int gg = 0; gg < 4; ++gg) {
                 const int r = gg >> 1, cc = gg & 1;
@@ -1562,10 +1574,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 float o[8];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                  o[i] = fmaf(vc[j0 + i], 1.f / (1 << tc::LOG2_LO), vm[j0 + i]) *
-                         (s_q[j * 64 + h * 32 + j0 + i] * s_c);
-                  o[4 + i] = fmaf(vc[j1 + i], 1.f / (1 << tc::LOG2_LO), vm[j1 + i]) *
-                             (s_q[j * 64 + h * 32 + j1 + i] * s_c);
+                  o[i] = vm[j0 + i] * tc::exp2_neg(e_q[j][h * 32 + j0 + i] + e_c);
+                  o[4 + i] = vm[j1 + i] * tc::exp2_neg(e_q[j][h * 32 + j1 + i] + e_c);
                 }
                 const int grp = (2 * h + r) * 2 + cc;
                 tc::st_global_v8(dst[j] + grp * plane, o);
@@ -1579,7 +1589,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           if (lane == 0) tcp::arrive(U(C.acc_empty[ab]));
         } else {
           tc::named_bar(2, 128);
-          if (ep == 0) arrive_remote(ab ? acc_empty_l1 : acc_empty_l0);
+          if (ep == 0) arrive_remote(acc_empty_base + ab * (uint32_t)sizeof(uint64_t));
         }
       }
       tcp::arrive(U(C.plan_empty[s]));
@@ -1823,14 +1833,17 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
   if ((st = check_launch("partial_plan")) != CVB_OK) return st;
   // cold iterations on SM pairs: every tile row of the range is whole
   const bool rows_whole = T.P.tile0 % T.P.tiles_x == 0 && T.P.ntile % T.P.tiles_x == 0;
-  if ((flags & CVB_TC_PAIRS) && !dbg && rows_whole && n_sms >= 2) {
+  // (CVB_TC_DEBUG: the single-tile debug kernel, or with bit 256 the pair
+  // kernel's debug instantiation)
+  if ((flags & CVB_TC_PAIRS) && (!dbg || (dbg & 256)) && rows_whole && n_sms >= 2) {
     const int64_t n_pairs = T.P.ntile / T.P.tiles_x * ((T.P.tiles_x + 1) / 2);
     const size_t smem2 = tcp2::smem_bytes();
-    static std::atomic<uint64_t> attr2{0};
-    ensure_max_smem(attr2, tcp2::pair_contract_kernel, (int)smem2);
+    auto kernel2 = dbg ? tcp2::pair_contract_kernel<true> : tcp2::pair_contract_kernel<false>;
+    static std::atomic<uint64_t> attr2{0}, attr2_dbg{0};
+    ensure_max_smem(dbg ? attr2_dbg : attr2, kernel2, (int)smem2);
     const int64_t max_cl = n_sms / 2;
     const int64_t grid2 = 2 * (n_pairs < max_cl ? n_pairs : max_cl);
-    launch_pdl(tcp2::pair_contract_kernel, dim3((unsigned)grid2), dim3(tcp::THREADS), smem2,
+    launch_pdl(kernel2, dim3((unsigned)grid2), dim3(tcp::THREADS), smem2,
                as_stream(stream), T, n_pairs);
     return check_launch("partial_contract_tcp2");
   }
