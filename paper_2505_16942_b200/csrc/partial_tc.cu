@@ -817,7 +817,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             dst = P.cache[cr.level] + tile * plane * TQH +
                   (int64_t)slot_of(cr.cy, cr.cx, ch, cw) * TQW;
           }
-          e_c = T.e2[cr.level][pair * T.pair_bytes[cr.level] + (int64_t)cr.cy * P.tw[cr.level] + cr.cx];
+          if (!(DEBUG && (T.dbg & 64)))
+            e_c = T.e2[cr.level][pair * T.pair_bytes[cr.level] + (int64_t)cr.cy * P.tw[cr.level] + cr.cx];
         }
         if (!__all_sync(0xffffffffu, WAIT_FULL(U(C.acc_full[ab]), cg >> 1))) goto done;
         tc::tc_fence_after();
@@ -908,6 +909,14 @@ __global__ void __launch_bounds__(PLAN_WARPS * 32) plan_kernel(PartialParams P) 
       if (v[h]) load_coord(P.coords, P.f64, tr.pix + (int64_t)py * P.w1 + px, x[h], y[h]);
     }
     const int nv = __popc(__ballot_sync(0xffffffffu, v[0])) + __popc(__ballot_sync(0xffffffffu, v[1]));
+    // lane l < L: its level's previous box, loaded now so the latency overlaps
+    // the anchor math
+    int32_t* meta = P.meta + (tile * P.levels + (lane < P.levels ? lane : 0)) * CVB_META_INTS;
+    int pm[5] = {0, 0, 0, 0, 0};
+    if (lane < P.levels) {
+#pragma unroll
+      for (int i = 0; i < 5; ++i) pm[i] = meta[i];
+    }
     int mylo_y = 0, myhi_y = 0, mylo_x = 0, myhi_x = 0;  // lane l keeps level l
     for (int l = 0; l < P.levels; ++l) {
       int ylo = INT_MAX, yhi = INT_MIN, xlo = INT_MAX, xhi = INT_MIN;
@@ -922,13 +931,11 @@ __global__ void __launch_bounds__(PLAN_WARPS * 32) plan_kernel(PartialParams P) 
           xhi = max(xhi, ax);
         }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        ylo = min(ylo, __shfl_xor_sync(0xffffffffu, ylo, o));
-        yhi = max(yhi, __shfl_xor_sync(0xffffffffu, yhi, o));
-        xlo = min(xlo, __shfl_xor_sync(0xffffffffu, xlo, o));
-        xhi = max(xhi, __shfl_xor_sync(0xffffffffu, xhi, o));
-      }
+      // warp reductions in one redux.sync each
+      ylo = __reduce_min_sync(0xffffffffu, ylo);
+      yhi = __reduce_max_sync(0xffffffffu, yhi);
+      xlo = __reduce_min_sync(0xffffffffu, xlo);
+      xhi = __reduce_max_sync(0xffffffffu, xhi);
       if (lane == l) {
         mylo_y = ylo;
         myhi_y = yhi;
@@ -937,12 +944,11 @@ __global__ void __launch_bounds__(PLAN_WARPS * 32) plan_kernel(PartialParams P) 
       }
     }
     int n_new = 0;
-    unsigned long long c_ovf = 0, c_empty = 0;
+    unsigned long long c_ovf = 0, c_empty = 0, c_dots, c_cells;
     int* rec = P.plans + tile * PLAN_INTS;
     if (lane < P.levels) {
       const int level = lane;
       const int th = P.th[level], tw = P.tw[level];
-      int32_t* meta = P.meta + (tile * P.levels + level) * CVB_META_INTS;
       Box B;
       B.ylo = max(mylo_y - r, 0);
       B.yhi = min(myhi_y + r + 1, th - 1);
@@ -955,8 +961,8 @@ __global__ void __launch_bounds__(PLAN_WARPS * 32) plan_kernel(PartialParams P) 
       } else if (B.h() > P.ch[level] || B.w() > P.cw[level]) {
         status = ST_OVERFLOW;
       }
-      const Box prev{meta[0], meta[1], meta[2], meta[3]};
-      const bool prev_ok = !P.no_cache && meta[4] == ST_OK && !prev.empty();
+      const Box prev{pm[0], pm[1], pm[2], pm[3]};
+      const bool prev_ok = !P.no_cache && pm[4] == ST_OK && !prev.empty();
       const Box I{max(B.ylo, prev.ylo), min(B.yhi, prev.yhi), max(B.xlo, prev.xlo),
                   min(B.xhi, prev.xhi)};
       const bool has_i = status == ST_OK && prev_ok && !I.empty();
@@ -986,14 +992,11 @@ __global__ void __launch_bounds__(PLAN_WARPS * 32) plan_kernel(PartialParams P) 
     if (lane <= P.levels) prefix[lane] = pre - n_new;       // exclusive prefix, lanes 0..L
     if (lane == P.levels) prefix[CVB_MAX_LEVELS + 1] = pre - n_new;  // n_cells
     if (lane == 0) prefix[CVB_MAX_LEVELS + 2] = (int)tile;           // the record's tile
-    unsigned long long c_dots = (unsigned long long)n_new * nv, c_cells = n_new;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      c_dots += __shfl_xor_sync(0xffffffffu, c_dots, o);
-      c_cells += __shfl_xor_sync(0xffffffffu, c_cells, o);
-      c_ovf += __shfl_xor_sync(0xffffffffu, c_ovf, o);
-      c_empty += __shfl_xor_sync(0xffffffffu, c_empty, o);
-    }
+    // per-warp totals (a tile's dots fit 32 bits: <= L * cap_h * cap_w * 64)
+    c_dots = __reduce_add_sync(0xffffffffu, (unsigned)(n_new * nv));
+    c_cells = __reduce_add_sync(0xffffffffu, (unsigned)n_new);
+    c_ovf = __reduce_add_sync(0xffffffffu, (unsigned)c_ovf);
+    c_empty = __reduce_add_sync(0xffffffffu, (unsigned)c_empty);
     if (lane == 0 && P.counters != nullptr) {
       if (c_dots) atomicAdd(&s_cnt[0], c_dots);
       if (c_cells) atomicAdd(&s_cnt[1], c_cells);
@@ -1116,9 +1119,22 @@ int* watchdog_word(cudaStream_t s) {
 // ---------------------------------------------------------------------------
 namespace tcp2 {
 
-using tcp::NST;
-using tcp::NBP;
-using tcp::NPL;
+// Rings of the pair kernel (A stages, F1 pieces, plan slots; the slots hold
+// only the pair's per-level tile plans, levels <= PMAXL).  5 A stages with 4
+// F1 pieces and 2 slots also fit 227 KB: no faster (A/B, round 2).
+#ifndef CVB_TC2_NST
+#define CVB_TC2_NST 4
+#endif
+#ifndef CVB_TC2_NBP
+#define CVB_TC2_NBP 5
+#endif
+#ifndef CVB_TC2_NPL
+#define CVB_TC2_NPL 3
+#endif
+constexpr int NST = CVB_TC2_NST;
+constexpr int NBP = CVB_TC2_NBP;
+constexpr int NPL = CVB_TC2_NPL;
+constexpr int PMAXL = 4;  // levels the pair kernel handles (more: single-tile kernel)
 using tcp::THREADS;
 using tcp::A_WARPS;
 using tcp::A_ROWS;
@@ -1176,11 +1192,11 @@ constexpr uint32_t IDESC2 = (1u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_
 
 // Work item: a pair of horizontally adjacent tiles (tile[1] < 0: a lone last
 // tile of an odd tile row) and the per-level hull of their boxes.
-struct PairSlot {
-  PlanRec rec[2];
-  int hull[CVB_MAX_LEVELS][4];  // ylo, yhi, xlo, xhi
-  int hw[CVB_MAX_LEVELS];       // hull width
-  int prefix[CVB_MAX_LEVELS + 1];
+struct alignas(16) PairSlot {
+  TilePlan plan[2][PMAXL];  // the two tiles' per-level plans (head of their PlanRecs)
+  int hull[PMAXL][4];       // ylo, yhi, xlo, xhi
+  int hw[PMAXL];            // hull width
+  int prefix[PMAXL + 1];
   int n_cells;
   int tile[2];
   int end;
@@ -1421,27 +1437,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         S.end = 0;
         S.tile[0] = t0;
         S.tile[1] = t1;
-        const uint32_t rec_bytes = (uint32_t)sizeof(PlanRec);
+        // the head of each PlanRec: its per-level TilePlans
+        const uint32_t rec_bytes = (uint32_t)(P.levels * sizeof(TilePlan));
         tc::mbar_expect_tx(U(C.plan_copy[s]), (rec_bytes + tc::N) * (t1 >= 0 ? 2 : 1));
-        tc::bulk_g2s(tc::smem_u32(&S.rec[0]), P.plans + (int64_t)t0 * PLAN_INTS, rec_bytes,
+        tc::bulk_g2s(tc::smem_u32(&S.plan[0][0]), P.plans + (int64_t)t0 * PLAN_INTS, rec_bytes,
                      U(C.plan_copy[s]));
         tc::bulk_g2s(tc::smem_u32(&C.e1[s][0][0]), T.e1 + (int64_t)t0 * tc::N, tc::N,
                      U(C.plan_copy[s]));
         if (t1 >= 0) {
-          tc::bulk_g2s(tc::smem_u32(&S.rec[1]), P.plans + (int64_t)t1 * PLAN_INTS, rec_bytes,
+          tc::bulk_g2s(tc::smem_u32(&S.plan[1][0]), P.plans + (int64_t)t1 * PLAN_INTS, rec_bytes,
                        U(C.plan_copy[s]));
           tc::bulk_g2s(tc::smem_u32(&C.e1[s][1][0]), T.e1 + (int64_t)t1 * tc::N, tc::N,
                        U(C.plan_copy[s]));
         }
         if (!WAIT_FULL2(U(C.plan_copy[s]), (uint32_t)(it / NPL))) goto done;
         int acc = 0;
-        for (int l = 0; l < CVB_MAX_LEVELS; ++l) {
+        for (int l = 0; l < PMAXL; ++l) {
           S.prefix[l] = acc;
           int ylo = INT_MAX, yhi = INT_MIN, xlo = INT_MAX, xhi = INT_MIN;
           if (l < P.levels) {
             for (int j = 0; j < 2; ++j) {
               if (j == 1 && t1 < 0) continue;
-              const TilePlan& tp = S.rec[j].plan[l];
+              const TilePlan& tp = S.plan[j][l];
               if (tp.status != ST_OK) continue;
               ylo = min(ylo, tp.B.ylo);
               yhi = max(yhi, tp.B.yhi);
@@ -1457,7 +1474,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           S.hw[l] = any ? xhi - xlo + 1 : 1;
           acc += any ? (yhi - ylo + 1) * (xhi - xlo + 1) : 0;
         }
-        S.prefix[CVB_MAX_LEVELS] = acc;
+        S.prefix[PMAXL] = acc;
         S.n_cells = acc;
         tcp::arrive(U(C.plan_full[s]));
       }
@@ -1550,12 +1567,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             if (S.tile[j] < 0) continue;
-            const TilePlan& tp = S.rec[j].plan[l];
+            const TilePlan& tp = S.plan[j][l];
             if (tp.status == ST_OK && in_box(tp.B, cy, cx))
               dst[j] = P.cache[l] + (int64_t)S.tile[j] * plane * TQH +
                        (int64_t)slot_of(cy, cx, ch, cw) * TQW;
           }
-          e_c = T.e2[l][pair * T.pair_bytes[l] + (int64_t)cy * P.tw[l] + cx];
+          if (!(DEBUG && (T.dbg & 64))) e_c = T.e2[l][pair * T.pair_bytes[l] + (int64_t)cy * P.tw[l] + cx];
         }
         if (!__all_sync(0xffffffffu, WAIT_FULL2(U(C.acc_full[ab]), cg / NACC))) goto done;
         tc::tc_fence_after();
@@ -1835,7 +1852,8 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
   const bool rows_whole = T.P.tile0 % T.P.tiles_x == 0 && T.P.ntile % T.P.tiles_x == 0;
   // (CVB_TC_DEBUG: the single-tile debug kernel, or with bit 256 the pair
   // kernel's debug instantiation)
-  if ((flags & CVB_TC_PAIRS) && (!dbg || (dbg & 256)) && rows_whole && n_sms >= 2) {
+  if ((flags & CVB_TC_PAIRS) && (!dbg || (dbg & 256)) && rows_whole && n_sms >= 2 &&
+      T.P.levels <= tcp2::PMAXL) {
     const int64_t n_pairs = T.P.ntile / T.P.tiles_x * ((T.P.tiles_x + 1) / 2);
     const size_t smem2 = tcp2::smem_bytes();
     auto kernel2 = dbg ? tcp2::pair_contract_kernel<true> : tcp2::pair_contract_kernel<false>;
