@@ -699,10 +699,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == 2) {
     // ---------------- plan loader: one bulk copy per tile record ----------------
     if (lane == 0) {
+      // dynamic tile scheduler; the next tile is claimed one record ahead, so
+      // the atomic's round trip overlaps the wait for a free slot
+      int64_t t_next = atomicAdd(tile_counter(P), 1);
       for (int64_t it = 0;; ++it) {
         const int s = (int)(it % NPL);
         if (!WAIT_EMPTY(U(C.plan_empty[s]), (uint32_t)(it / NPL))) goto done;
-        const int64_t t = atomicAdd(tile_counter(P), 1);  // dynamic tile scheduler
+        const int64_t t = t_next;
+        if (t < P.ntile) t_next = atomicAdd(tile_counter(P), 1);
         if (t >= P.ntile) {  // end of the work list: a sentinel record
           C.slot[s].tile = -1;
           arrive(U(C.plan_full[s]));
@@ -1410,15 +1414,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   } else if (warp == 2) {
     // ---------------- plan loader: both tiles' records + the per-level hull ----------------
     if (lane == 0) {
+      // dynamic pair scheduling: the leader claims pairs (one ahead, so the
+      // atomic's round trip overlaps the slot wait) and posts each index into
+      // the follower's mailbox for the same slot
+      int64_t pidx_next = leader ? atomicAdd(tcp::tile_counter(P), 1) : 0;  // reset by plan_kernel
       for (int64_t it = 0;; ++it) {
         const int s = (int)(it % NPL);
         if (!WAIT_EMPTY2(U(C.plan_empty[s]), (uint32_t)(it / NPL))) goto done;
         PairSlot& S = C.slot[s];
-        // dynamic pair scheduling: the leader claims the next pair and posts
-        // its index into the follower's mailbox for the same slot
         int64_t pidx;
         if (leader) {
-          pidx = atomicAdd(tcp::tile_counter(P), 1);  // reset by plan_kernel
+          pidx = pidx_next;
+          if (pidx < n_pairs) pidx_next = atomicAdd(tcp::tile_counter(P), 1);
           st_cluster_u64(mapa(tc::smem_u32(&C.pidx[s]), 1), (unsigned long long)pidx);
           asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
                            mapa(U(C.pidx_full[s]), 1))

@@ -1,4 +1,4 @@
-# usage (GPU box): bash scripts/gpu_evidence_r2.sh TAG — round-2 evidence: launch list, full
+# usage (GPU box): bash scripts/gpu_evidence_r2.sh TAG — round-2 (final build) evidence: launch list, full
 # captures (C4 warm + cold, C1-C3 warm traffic, dense / on-demand / strict kernels), sanitizer
 cd ${GRAFT_REPO_ROOT:-.}
 TAG=${1:-e}
@@ -12,7 +12,7 @@ timeout 900 $NCU --set full --clock-control none --import-source on \
   -o gpurun_out/prof_warm_C4_$TAG python bench.py --profile-only --steps 1 --warmup 0 > gpurun_out/ncu_warm_C4_$TAG.log 2>&1
 echo warm C4 rc $?
 timeout 900 $NCU --set full --clock-control none --import-source on \
-  -k regex:"partial_contract_tcp_kernel|split_f1_kernel|split_level_kernel|plan_kernel" -c 7 \
+  -k regex:"pair_contract_kernel|split_f1_kernel|split_level_kernel|plan_kernel" -c 6 \
   -o gpurun_out/prof_cold_C4_$TAG python bench.py --profile-only --steps 1 --warmup 0 > gpurun_out/ncu_cold_C4_$TAG.log 2>&1
 echo cold C4 rc $?
 for C in C1 C2 C3; do
