@@ -22,9 +22,6 @@
 // products, the warp cooperating on each query's window (gather.cu semantics).
 #include <stdlib.h>
 
-#include <stddef.h>
-#include <type_traits>
-
 #include "partial.cuh"
 
 namespace cvb {
@@ -42,25 +39,6 @@ struct Shared {
   float outs[WARPS][QG * MAXL * KK];   // 10,368 B per warp
   float patch[WARPS][S * S];           // overflow path: one query's window
 };
-
-// Staged variant: per level, the group's union window (the 8 queries'
-// windows, <= MAXC cells) is copied into shared memory one 32-byte cell
-// (the group's 8 costs, one cache sector) per lane and 256-bit load — one L1
-// request per cell instead of one per (query, tap) — and the taps are
-// combined from there.  Groups with a larger window use the register-direct
-// path.
-constexpr int MAXC = 192;
-struct SharedStaged {
-  float outs[WARPS][QG * MAXL * KK];
-  float patch[WARPS][S * S];
-  float4 stage[WARPS][MAXC * 2];       // 6,144 B per warp: [cell][8 queries]
-};
-
-__device__ __forceinline__ void ld_sector(const float* p, float4& a, float4& b) {
-  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
-      : "l"(p));
-}
 
 // Overflowed tile-level (its box exceeded the cache window): the warp
 // evaluates each query's (2r+2)^2 window by direct dot products — lanes split
@@ -123,12 +101,10 @@ __device__ __noinline__ void overflow_level(const float* f1, const float* f2, in
   }
 }
 
-template <bool STAGED>
-__global__ void __launch_bounds__(WARPS * 32, STAGED ? 6 : 16 / WARPS)
-    gather_fast_kernel(PartialParams P, float* out, int level0, int nlev) {
+__global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(PartialParams P, float* out,
+                                                                    int level0, int nlev) {
   extern __shared__ __align__(16) uint8_t g_smem[];
-  using SM = typename std::conditional<STAGED, SharedStaged, Shared>::type;
-  SM& sm = *reinterpret_cast<SM*>(g_smem);
+  Shared& sm = *reinterpret_cast<Shared*>(g_smem);
   pdl_trigger();
   pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -175,113 +151,9 @@ __global__ void __launch_bounds__(WARPS * 32, STAGED ? 6 : 16 / WARPS)
                      P.th[level0 + l_], P.tw[level0 + l_], P.d, P.vec,
                      pix0, P.w1, vmask, ay, ax, w, l_, nlev, sm.patch[warp], O, lane);
   }
-  bool staged = false;
-  int wy0 = 0, wx0 = 0, wh = 0, ww = 0;  // lane (q, l): level l's union window
-  if (STAGED) {
-    int ylo = qvalid ? ay : INT_MAX, yhi = qvalid ? ay : INT_MIN;
-    int xlo = qvalid ? ax : INT_MAX, xhi = qvalid ? ax : INT_MIN;
-#pragma unroll
-    for (int o = 1; o < QG; o <<= 1) {  // over the 8 lanes of the level
-      ylo = min(ylo, __shfl_xor_sync(0xffffffffu, ylo, o));
-      yhi = max(yhi, __shfl_xor_sync(0xffffffffu, yhi, o));
-      xlo = min(xlo, __shfl_xor_sync(0xffffffffu, xlo, o));
-      xhi = max(xhi, __shfl_xor_sync(0xffffffffu, xhi, o));
-    }
-    wy0 = ylo - R;
-    wx0 = xlo - R;
-    wh = yhi - ylo + S;
-    ww = xhi - xlo + S;
-    staged = __all_sync(0xffffffffu, status != ST_OK || li >= nlev || wh * ww <= MAXC);
-  }
-  if (staged) {
-    float4* st4 = reinterpret_cast<float4*>(g_smem + offsetof(SharedStaged, stage)) + warp * MAXC * 2;
-    const float* stage = reinterpret_cast<const float*>(st4);
-    const int qq = lane & 7, part = lane >> 3;
-    const int r0 = part == 0 ? 0 : 2 * part + 1, nr = part == 0 ? 3 : 2;  // tap rows 0-2,3-4,5-6,7-8
-    // empty levels: zero taps
-    for (int l_ = 0; l_ < nlev; ++l_) {
-      const int st = __shfl_sync(0xffffffffu, status, 8 * l_);
-      if (st != ST_OK && st != ST_OVERFLOW)
-        for (int e = lane; e < QG * KK; e += 32) O[((e / KK) * nlev + l_) * KK + e % KK] = 0.f;
-    }
-    // ST_OK levels in order; level l+1's sectors are loaded into registers
-    // while level l's taps are combined from shared memory
-    unsigned okmask = 0;
-    for (int l_ = 0; l_ < nlev; ++l_)
-      if (__shfl_sync(0xffffffffu, status, 8 * l_) == ST_OK) okmask |= 1u << l_;
-    constexpr int PER_LANE = MAXC / 32;
-    float4 va[PER_LANE], vb[PER_LANE];
-    auto load_level = [&](int l_) {
-      const int l = level0 + l_;
-      const int y0 = __shfl_sync(0xffffffffu, wy0, 8 * l_), x0 = __shfl_sync(0xffffffffu, wx0, 8 * l_);
-      const int hh = __shfl_sync(0xffffffffu, wh, 8 * l_), wd = __shfl_sync(0xffffffffu, ww, 8 * l_);
-      const int th = P.th[l], tw = P.tw[l], ch = P.ch[l], cw = P.cw[l];
-      const float* plane = P.cache[l] + ((tile * QG + grp) * (int64_t)(ch * cw)) * QG;
-      const int ncell = hh * wd;
-#pragma unroll
-      for (int k = 0; k < PER_LANE; ++k) {
-        const int c = lane + 32 * k;
-        va[k] = vb[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (c < ncell) {
-          const int r = c / wd, col = c - r * wd;
-          const int cy = y0 + r, cx = x0 + col;
-          if (cy >= 0 && cy < th && cx >= 0 && cx < tw)
-            ld_sector(plane + (int64_t)((cy % ch) * cw + cx % cw) * QG, va[k], vb[k]);
-        }
-      }
-    };
-    int l_ = okmask ? __ffs(okmask) - 1 : nlev;
-    if (l_ < nlev) load_level(l_);
-    while (l_ < nlev) {
-      const int y0 = __shfl_sync(0xffffffffu, wy0, 8 * l_), x0 = __shfl_sync(0xffffffffu, wx0, 8 * l_);
-      const int hh = __shfl_sync(0xffffffffu, wh, 8 * l_), wd = __shfl_sync(0xffffffffu, ww, 8 * l_);
-#pragma unroll
-      for (int k = 0; k < PER_LANE; ++k) {
-        const int c = lane + 32 * k;
-        if (c < hh * wd) {
-          st4[2 * c] = va[k];
-          st4[2 * c + 1] = vb[k];
-        }
-      }
-      __syncwarp();
-      const unsigned rest = okmask & ~((2u << l_) - 1u);
-      const int nxt = rest ? __ffs(rest) - 1 : nlev;
-      if (nxt < nlev) load_level(nxt);  // in flight during this level's taps
-      // lane (qq, part): query qq's tap rows r0 .. r0+nr-1 at this level
-      const int src = qq + 8 * l_;
-      const int qay = __shfl_sync(0xffffffffu, ay, src), qax = __shfl_sync(0xffffffffu, ax, src);
-      Weights32 qw;
-      qw.w00 = __shfl_sync(0xffffffffu, w.w00, src);
-      qw.w01 = __shfl_sync(0xffffffffu, w.w01, src);
-      qw.w10 = __shfl_sync(0xffffffffu, w.w10, src);
-      qw.w11 = __shfl_sync(0xffffffffu, w.w11, src);
-      if ((vmask >> qq) & 1u) {
-        const float* sq = stage + qq + ((qay - R - y0 + r0) * wd + (qax - R - x0)) * QG;
-        float prev[S], cur[S];
-#pragma unroll
-        for (int i = 0; i < S; ++i) prev[i] = sq[i * QG];
-        float* o = O + (qq * nlev + l_) * KK + r0 * K;
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          if (j < nr) {
-            const float* row = sq + (j + 1) * wd * QG;
-#pragma unroll
-            for (int i = 0; i < S; ++i) cur[i] = row[i * QG];
-#pragma unroll
-            for (int i = 0; i < K; ++i)
-              o[j * K + i] = combine32(prev[i], prev[i + 1], cur[i], cur[i + 1], qw);
-#pragma unroll
-            for (int i = 0; i < S; ++i) prev[i] = cur[i];
-          }
-        }
-      }
-      __syncwarp();
-      l_ = nxt;
-    }
-  }
   // every lane (q, l) combines the 81 taps of query q at level l, three tap
   // rows per pass from 4 x 10 cache values loaded into registers
-  if (!staged && li < nlev && qvalid && status != ST_OVERFLOW) {
+  if (li < nlev && qvalid && status != ST_OVERFLOW) {
     const int l = level0 + li;
     const int th = P.th[l], tw = P.tw[l], ch = P.ch[l], cw = P.cw[l];
     const float* plane = P.cache[l] + ((tile * QG + grp) * (int64_t)(ch * cw)) * QG + q;
@@ -376,35 +248,28 @@ __global__ void __launch_bounds__(WARPS * 32, STAGED ? 6 : 16 / WARPS)
 }  // namespace gfast
 
 int launch_gather_fast_r4(const PartialParams& P, float* out, cudaStream_t s) {
-  // CVB_GF_STAGED=1: the shared-memory staged taps (A/B)
-  static int staged = -1;
-  if (staged < 0) {
-    const char* e = getenv("CVB_GF_STAGED");
-    staged = e && atoi(e) != 0;
-  }
-  auto kernel = staged ? gfast::gather_fast_kernel<true> : gfast::gather_fast_kernel<false>;
-  static std::atomic<uint64_t> attr{0}, attr_st{0};
-  const int smem = (int)(staged ? sizeof(gfast::SharedStaged) : sizeof(gfast::Shared));
-  ensure_max_smem(staged ? attr_st : attr, kernel, smem);
+  static std::atomic<uint64_t> attr{0};
+  const int smem = (int)sizeof(gfast::Shared);
+  ensure_max_smem(attr, gfast::gather_fast_kernel, smem);
   // Shared-memory carveout 65%: the taps re-read each cache sector ~3x through
   // L1, so L1 capacity matters more than the last CTA slot per SM (measured:
   // 65% is 1-2% faster than the default 200 KB carveout; 100% halves the
   // speed).  CVB_GF_CARVEOUT overrides (percent; -1 = driver default).
-  static std::atomic<uint64_t> carved{0}, carved_st{0};
+  static std::atomic<uint64_t> carved{0};
   int dev = 0;
   cudaGetDevice(&dev);
   const uint64_t bit = 1ull << (dev & 63);
-  std::atomic<uint64_t>& cv = staged ? carved_st : carved;
-  if (!(cv.load() & bit)) {
+  if (!(carved.load() & bit)) {
     const char* e = getenv("CVB_GF_CARVEOUT");
     const int carve = e ? atoi(e) : 65;
     if (carve >= 0)
-      cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-    cv.fetch_or(bit);
+      cudaFuncSetAttribute(gfast::gather_fast_kernel,
+                           cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+    carved.fetch_or(bit);
   }
   for (int l0 = 0; l0 < P.levels; l0 += gfast::MAXL) {
     const int nl = min(gfast::MAXL, P.levels - l0);
-    launch_pdl(kernel, dim3((unsigned)(gfast::CTAS_PER_TILE * P.ntile)), dim3(gfast::WARPS * 32), smem,
+    launch_pdl(gfast::gather_fast_kernel, dim3((unsigned)(gfast::CTAS_PER_TILE * P.ntile)), dim3(gfast::WARPS * 32), smem,
                s, P, out, l0, nl);
     const int st = check_launch("partial_gather_fast");
     if (st != CVB_OK) return st;
