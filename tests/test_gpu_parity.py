@@ -390,6 +390,27 @@ def test_pipelined_tile_ranges_equal_single_launch(cuda):
         assert O.deviation(b, want, want) <= REF_GATE
 
 
+@pytest.mark.parametrize("levels,radius", [(5, 4), (6, 3)])
+def test_more_levels_than_one_sampler_launch(cuda, levels, radius):
+    """Pyramids deeper than the SM-pair kernel and one fast-sampler launch take
+    (4 levels): the cold iteration on the single-tile kernel, the r=4 sampler
+    in two launches (levels 0-3, then the rest), the generic-radius sampler
+    for r=3.  Strict bit for bit, fast within both gates, every iteration."""
+    spec = cvb.LookupSpec(radius, levels)
+    sc = cvb.gen_scenario(11, (96, 160, 64), 4, spec, coords_dtype=np.float32)
+    f1 = cvb.FeatureMap(torch.from_numpy(sc.f1).to(cuda))
+    f2 = cvb.FeatureMap(torch.from_numpy(sc.f2).to(cuda))
+    strict = cvb.CorrSampler(f1, f2, spec, strict=True)
+    fast = cvb.CorrSampler(f1, f2, spec)
+    assert fast.state.tc
+    for coords in sc.centroid_fields:
+        want = O.lookup(sc.f1, sc.f2, coords, radius, levels)
+        c = cvb.CentroidField(torch.from_numpy(coords).to(cuda))
+        assert np.array_equal(strict(c).numpy(), want)
+        dev, ns = _gates(fast(c).numpy(), want, sc.f1, sc.f2)
+        assert dev <= REF_GATE and ns <= NS_GATE
+
+
 def test_tc_per_row_scaling_wide_dynamic_range(cuda):
     """Rows spanning 2^-20 .. 2^20 in magnitude: every row carries its own
     power-of-two scale through the fp16 split, so both gates hold per row."""
