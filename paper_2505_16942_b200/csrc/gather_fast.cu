@@ -102,13 +102,18 @@ __device__ __noinline__ void overflow_level(const float* f1, const float* f2, in
 }
 
 __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(PartialParams P, float* out,
-                                                                    int level0, int nlev) {
+                                                                    int level0, int nlev,
+                                                                    bool reverse) {
   extern __shared__ __align__(16) uint8_t g_smem[];
   Shared& sm = *reinterpret_cast<Shared*>(g_smem);
   pdl_trigger();
   pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tile = P.tile0 + blockIdx.x / CTAS_PER_TILE;
+  // tiles in reverse order: the contraction claims tiles in increasing order,
+  // so the last tiles' new cells are the likeliest to still be in L2 (-1.1%
+  // per C4 step, A/B; CVB_GF_REVERSE=0 restores the forward order)
+  const int64_t ti = blockIdx.x / CTAS_PER_TILE;
+  const int64_t tile = P.tile0 + (reverse ? P.ntile - 1 - ti : ti);
   const TileRef tr = tile_ref(P, tile);
   const int tile_y = tr.ty, tile_x = tr.tx;
   // query group: tile rows 2(g>>1)..+1, columns 4(g&1)..+3
@@ -249,6 +254,11 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
 
 int launch_gather_fast_r4(const PartialParams& P, float* out, cudaStream_t s) {
   static std::atomic<uint64_t> attr{0};
+  static int reverse = -1;
+  if (reverse < 0) {
+    const char* e = getenv("CVB_GF_REVERSE");
+    reverse = !e || atoi(e) != 0;
+  }
   const int smem = (int)sizeof(gfast::Shared);
   ensure_max_smem(attr, gfast::gather_fast_kernel, smem);
   // Shared-memory carveout 65%: the taps re-read each cache sector ~3x through
@@ -270,7 +280,7 @@ int launch_gather_fast_r4(const PartialParams& P, float* out, cudaStream_t s) {
   for (int l0 = 0; l0 < P.levels; l0 += gfast::MAXL) {
     const int nl = min(gfast::MAXL, P.levels - l0);
     launch_pdl(gfast::gather_fast_kernel, dim3((unsigned)(gfast::CTAS_PER_TILE * P.ntile)), dim3(gfast::WARPS * 32), smem,
-               s, P, out, l0, nl);
+               s, P, out, l0, nl, reverse != 0);
     const int st = check_launch("partial_gather_fast");
     if (st != CVB_OK) return st;
   }
