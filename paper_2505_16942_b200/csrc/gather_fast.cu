@@ -10,8 +10,9 @@
 //     launch); lane
 //     (q, l) = (lane & 7, lane >> 3) derives the anchor and weights of query
 //     q at level l once (the four levels in parallel);
-//   * taps: lane (q, l) owns query q at level l: three passes of 3 tap rows,
-//     each loading the 4 x 10 patch values it needs from the cache plane
+//   * taps: lane (q, l) owns query q at level l: two passes of 5 and 4 tap
+//     rows, each loading the 6 x 10 / 4 x 10 patch values it needs from the
+//     cache plane
 //     ([slot][8 queries], 32-byte sectors shared by the row's queries through
 //     L1) into registers, zero outside the level grid, and combining them
 //     (canonical fp32 combine, pre-scaled weights);
@@ -101,9 +102,9 @@ __device__ __noinline__ void overflow_level(const float* f1, const float* f2, in
   }
 }
 
-__global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(PartialParams P, float* out,
-                                                                    int level0, int nlev,
-                                                                    bool reverse) {
+template <int NPASS>
+__global__ void __launch_bounds__(WARPS * 32, NPASS >= 3 ? 16 / WARPS : (NPASS == 2 ? 7 : 6))
+    gather_fast_kernel(PartialParams P, float* out, int level0, int nlev, bool reverse) {
   extern __shared__ __align__(16) uint8_t g_smem[];
   Shared& sm = *reinterpret_cast<Shared*>(g_smem);
   pdl_trigger();
@@ -156,8 +157,8 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
                      P.th[level0 + l_], P.tw[level0 + l_], P.d, P.vec,
                      pix0, P.w1, vmask, ay, ax, w, l_, nlev, sm.patch[warp], O, lane);
   }
-  // every lane (q, l) combines the 81 taps of query q at level l, three tap
-  // rows per pass from 4 x 10 cache values loaded into registers
+  // every lane (q, l) combines the 81 taps of query q at level l, TPP tap
+  // rows per pass from (TPP + 1) x 10 cache values loaded into registers
   if (li < nlev && qvalid && status != ST_OVERFLOW) {
     const int l = level0 + li;
     const int th = P.th[l], tw = P.tw[l], ch = P.ch[l], cw = P.cw[l];
@@ -175,21 +176,25 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
       if (++xs == cw) xs = 0;
     }
     float* o = O + (q * nlev + li) * KK;
-    // patch rows 0-3, then 4-6 and 7-9: a pass's last row is the next pass's
-    // first, carried in registers (each cache row is loaded once)
-    float v[4][S];
+    // NPASS passes of TPP tap rows (TPP + 1 patch rows in registers): a pass's
+    // last row is the next pass's first, carried in registers (each cache row
+    // is loaded once); fewer passes = fewer dependent load round trips, more
+    // registers
+    constexpr int TPP = (K + NPASS - 1) / NPASS;
+    float v[TPP + 1][S];
     int sy = (ay - R) % ch;
     if (sy < 0) sy += ch;
 #pragma unroll 1
-    for (int pass = 0; pass < 3; ++pass) {
-      const int y0 = ay - R + 3 * pass;
+    for (int pass = 0; pass < NPASS; ++pass) {
+      const int t0 = TPP * pass, nt = min(TPP, K - t0);
+      const int y0 = ay - R + t0;
       if (pass > 0) {
 #pragma unroll
-        for (int i = 0; i < S; ++i) v[0][i] = v[3][i];
+        for (int i = 0; i < S; ++i) v[0][i] = v[TPP][i];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (pass > 0 && j == 0) continue;
+      for (int j = 0; j <= TPP; ++j) {
+        if ((pass > 0 && j == 0) || j > nt) continue;
         const int gy = y0 + j;
         const bool rin = status == ST_OK && gy >= 0 && gy < th;
         const float* prow = plane + (int64_t)(sy * cw) * QG;
@@ -198,11 +203,11 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
         if (++sy == ch) sy = 0;
       }
 #pragma unroll
-      for (int j = 0; j < 3; ++j)
+      for (int j = 0; j < TPP; ++j)
+        if (j < nt)
 #pragma unroll
-        for (int i = 0; i < K; ++i)
-          o[(3 * pass + j) * K + i] =
-              combine32(v[j][i], v[j][i + 1], v[j + 1][i], v[j + 1][i + 1], w);
+          for (int i = 0; i < K; ++i)
+            o[(t0 + j) * K + i] = combine32(v[j][i], v[j][i + 1], v[j + 1][i], v[j + 1][i + 1], w);
     }
   }
   __syncwarp();
@@ -253,6 +258,17 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) gather_fast_kernel(Par
 }  // namespace gfast
 
 int launch_gather_fast_r4(const PartialParams& P, float* out, cudaStream_t s) {
+  // tap-row passes per query: 2 (patch rows 0-5, then 5-9; 128 registers,
+  // the same 16 warps per SM as 3 passes of 3 rows, one dependent load round
+  // trip fewer: -1.8% sampler time at C4, A/B); CVB_GF_PASSES=1|3 for A/B
+  static int npass = -1;
+  if (npass < 0) {
+    const char* e = getenv("CVB_GF_PASSES");
+    npass = e ? atoi(e) : 2;
+    if (npass != 1 && npass != 3) npass = 2;
+  }
+  auto kernel = npass == 1 ? gfast::gather_fast_kernel<1>
+                           : (npass == 2 ? gfast::gather_fast_kernel<2> : gfast::gather_fast_kernel<3>);
   static std::atomic<uint64_t> attr{0};
   static int reverse = -1;
   if (reverse < 0) {
@@ -260,7 +276,7 @@ int launch_gather_fast_r4(const PartialParams& P, float* out, cudaStream_t s) {
     reverse = !e || atoi(e) != 0;
   }
   const int smem = (int)sizeof(gfast::Shared);
-  ensure_max_smem(attr, gfast::gather_fast_kernel, smem);
+  ensure_max_smem(attr, kernel, smem);
   // Shared-memory carveout 65%: the taps re-read each cache sector ~3x through
   // L1, so L1 capacity matters more than the last CTA slot per SM (measured:
   // 65% is 1-2% faster than the default 200 KB carveout; 100% halves the
@@ -273,13 +289,12 @@ int launch_gather_fast_r4(const PartialParams& P, float* out, cudaStream_t s) {
     const char* e = getenv("CVB_GF_CARVEOUT");
     const int carve = e ? atoi(e) : 65;
     if (carve >= 0)
-      cudaFuncSetAttribute(gfast::gather_fast_kernel,
-                           cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+      cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
     carved.fetch_or(bit);
   }
   for (int l0 = 0; l0 < P.levels; l0 += gfast::MAXL) {
     const int nl = min(gfast::MAXL, P.levels - l0);
-    launch_pdl(gfast::gather_fast_kernel, dim3((unsigned)(gfast::CTAS_PER_TILE * P.ntile)), dim3(gfast::WARPS * 32), smem,
+    launch_pdl(kernel, dim3((unsigned)(gfast::CTAS_PER_TILE * P.ntile)), dim3(gfast::WARPS * 32), smem,
                s, P, out, l0, nl, reverse != 0);
     const int st = check_launch("partial_gather_fast");
     if (st != CVB_OK) return st;

@@ -13,8 +13,7 @@
 //     128-row B matrix: main += hi.hi and corr += hi.lo, reading A_hi from
 //     shared memory once) and one N=64 MMA (corr += lo.hi) keep ~22
 //     significant bits per product (products of two fp16 are exact in the
-//     fp32 accumulator; the SM-pair kernel sums all three into one
-//     accumulator);
+//     fp32 accumulator);
 //   * operands are pre-split once per image pair (cvb_tc_prepare): the F1
 //     tile is a contiguous image of its shared-memory layout cut into K
 //     pieces of 64 channels (16 KB: hi 8 KB + lo 8 KB), each fetched with one
@@ -46,8 +45,8 @@ constexpr int A_STAGE = 2 * A_HALF;      // 32 KB
 constexpr int B_HALF = N * KP * 2;       // 8 KB (hi or lo)
 constexpr int B_PIECE = 2 * B_HALF;      // 16 KB
 constexpr int MAX_DP = 256;
-// lo = fp16(x - hi), unscaled: the hi.lo and lo.hi products have the scale
-// of hi.hi, so they may share its accumulator (the SM-pair kernel does)
+// lo = fp16(x - hi), unscaled: main (hi.hi) + corr (hi.lo + lo.hi) is a plain
+// add in the epilogue
 constexpr int TARGET_EXP = 14;           // max |x * 2^e| < 2^14
 
 // instruction descriptor: D f32, A/B f16, both K-major, N=64, M=128
@@ -1108,12 +1107,9 @@ int* watchdog_word(cudaStream_t s) {
 // hull of their two boxes once, as M=256 chunks: each CTA gathers half of
 // every chunk's cell rows (A) and holds its own tile's F1 image (B = the two
 // tiles' 128 queries, N-split across the CTAs); the leader CTA issues
-// tcgen05.mma.cta_group::2 (A_hi.B_hi + A_hi.B_lo + A_lo.B_hi, three N=128
-// MMAs per K=16 step into ONE accumulator: lo is unscaled, so the products
-// share a scale and the epilogue reads 128 TMEM columns per chunk instead of
-// 256 — TMEM reads, ~64 B/clk/SM, paced the epilogue) and every commit is
-// multicast to both CTAs' barriers.  Each CTA's TMEM holds its 128 cells x
-// 128 queries in a 4-deep accumulator ring; its
+// tcgen05.mma.cta_group::2 (main = A_hi.B_hi, corr = A_hi.B_lo + A_lo.B_hi,
+// three N=128 MMAs per K=16 step) and every commit is multicast to both
+// CTAs' barriers.  Each CTA's TMEM holds its 128 cells x 128 queries; its
 // epilogue writes every cell that lies in tile j's box into tile j's cache
 // (the same cells the single-tile kernel writes when the tile is cold; a
 // cell of the previous box is rewritten with its own value when it is not).
@@ -1144,9 +1140,12 @@ using tcp::A_WARPS;
 using tcp::A_ROWS;
 
 constexpr int M2 = 256;  // cells per pair chunk (128 per CTA)
-// one fp32 accumulator per chunk (hi.hi + hi.lo + lo.hi share a scale: lo
-// is unscaled): 128 TMEM columns per buffer, a 4-deep ring in 512 columns
-constexpr int NACC = 4;
+// accumulators: main (hi.hi) and corr (hi.lo + lo.hi) in 128 TMEM columns
+// each per buffer, a 2-deep ring in 512 columns — the same two sums in the
+// same order as the single-tile kernel, so a cell has the same bits whichever
+// kernel computed it (one shared accumulator: 3% faster here, but not
+// bit-compatible with the single-tile kernel's cells)
+constexpr int NACC = 2;
 constexpr int RELAY_LANES = NST + 1;  // follower relay: one lane per A stage + one for B
 
 __device__ __forceinline__ uint32_t cta_rank() {
@@ -1343,7 +1342,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             const int ab = (int)(cg % NACC);
             if (!__all_sync(0xffffffffu, WAIT_EMPTY_CL(U(C.acc_empty[ab]), cg / NACC))) goto done;
             tc::tc_fence_after();
-            const uint32_t d_acc = tmem + ab * 128;
+            const uint32_t d_main = tmem + ab * 256, d_corr = d_main + 128;
             for (int kb = 0; kb < n_kb; ++kb, ++g) {
               const uint32_t pi = pb + kb;
               const int bs = (int)(pi % NBP);
@@ -1362,9 +1361,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 for (int k = 0; k < tc::KP / 16; ++k) {
                   if (DEBUG && (T.dbg & 4)) break;
                   const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-                  mma2<IDESC2>(d_acc, dah + 2 * k, dbh + 16 * k, acc);  // A_hi B_hi
-                  mma2<IDESC2>(d_acc, dah + 2 * k, dbl + 16 * k, 1u);   // A_hi B_lo
-                  mma2<IDESC2>(d_acc, dal + 2 * k, dbh + 16 * k, 1u);   // A_lo B_hi
+                  mma2<IDESC2>(d_main, dah + 2 * k, dbh + 16 * k, acc);  // A_hi B_hi
+                  mma2<IDESC2>(d_corr, dah + 2 * k, dbl + 16 * k, acc);  // A_hi B_lo
+                  mma2<IDESC2>(d_corr, dal + 2 * k, dbh + 16 * k, 1u);   // A_lo B_hi
                 }
                 commit_mc(U(C.a_empty[st]));
                 if (c == n_chunks - 1) commit_mc(U(C.b_empty[bs]));
@@ -1583,13 +1582,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         if (!__all_sync(0xffffffffu, WAIT_FULL2(U(C.acc_full[ab]), cg / NACC))) goto done;
         tc::tc_fence_after();
-        float vm[32];
+        float vm[32], vc[32];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const uint32_t col = (uint32_t)(j * 64 + h * 32);
-            tc::tmem_ld32(tmem + ab * 128 + lane_base + col, vm);
+            tc::tmem_ld32(tmem + ab * 256 + lane_base + col, vm);
+            tc::tmem_ld32(tmem + ab * 256 + 128 + lane_base + col, vc);
             if (dst[j] != nullptr && !(DEBUG && (T.dbg & 2))) {
 #pragma unroll
               for (int gg = 0; gg < 4; ++gg) {
@@ -1598,8 +1598,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 float o[8];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                  o[i] = vm[j0 + i] * tc::exp2_neg(e_q[j][h * 32 + j0 + i] + e_c);
-                  o[4 + i] = vm[j1 + i] * tc::exp2_neg(e_q[j][h * 32 + j1 + i] + e_c);
+                  o[i] = (vm[j0 + i] + vc[j0 + i]) * tc::exp2_neg(e_q[j][h * 32 + j0 + i] + e_c);
+                  o[4 + i] = (vm[j1 + i] + vc[j1 + i]) * tc::exp2_neg(e_q[j][h * 32 + j1 + i] + e_c);
                 }
                 const int grp = (2 * h + r) * 2 + cc;
                 tc::st_global_v8(dst[j] + grp * plane, o);
