@@ -102,24 +102,39 @@ __device__ __noinline__ void overflow_level(const float* f1, const float* f2, in
   }
 }
 
-// One query group (2 x 4 queries) at levels level0 .. level0+nlev-1, called
-// by a whole warp: (x, y) are lane (q, l)'s query coordinates (q = lane & 7),
-// `status` is its level's tile-level status.
 template <int NPASS>
-__device__ __forceinline__ void sample_group(const PartialParams& P, float* out, int level0, int nlev,
-                                             int64_t tile, const TileRef& tr, int grp, int py0,
-                                             int px0, double x, double y, int status, float* O,
-                                             float* patch, int lane) {
+__global__ void __launch_bounds__(WARPS * 32, NPASS >= 3 ? 16 / WARPS : (NPASS == 2 ? 7 : 6))
+    gather_fast_kernel(PartialParams P, float* out, int level0, int nlev, bool reverse) {
+  extern __shared__ __align__(16) uint8_t g_smem[];
+  Shared& sm = *reinterpret_cast<Shared*>(g_smem);
+  pdl_trigger();
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // tiles in reverse order: the contraction claims tiles in increasing order,
+  // so the last tiles' new cells are the likeliest to still be in L2 (-1.1%
+  // per C4 step, A/B; CVB_GF_REVERSE=0 restores the forward order)
+  const int64_t ti = blockIdx.x / CTAS_PER_TILE;
+  const int64_t tile = P.tile0 + (reverse ? P.ntile - 1 - ti : ti);
+  const TileRef tr = tile_ref(P, tile);
+  const int tile_y = tr.ty, tile_x = tr.tx;
+  // query group: tile rows 2(g>>1)..+1, columns 4(g&1)..+3
+  const int grp = (int)(blockIdx.x % CTAS_PER_TILE) * WARPS + warp;
+  const int py0 = tile_y * TQH + group_qy(grp, 0), px0 = tile_x * TQW + group_qx(grp, 0);
+  if (py0 >= P.h1) return;  // warp-uniform
+
   // ---- lane (q, l): anchor, fractions and weights of query q at level l ----
   const int q = lane & 7, li = lane >> 3;
   const int py = py0 + (q >> 2), px = px0 + (q & 3);
   const bool qvalid = py < P.h1 && px < P.w1;
   const unsigned vmask = __ballot_sync(0xffffffffu, qvalid) & 0xFFu;
-  int ay = 0, ax = 0;
+  int ay = 0, ax = 0, status = ST_EMPTY;
   Weights32 w{0.f, 0.f, 0.f, 0.f};
   if (li < nlev) {
     const int l = level0 + li;
+    status = P.meta[(tile * P.levels + l) * CVB_META_INTS + 4];
     if (qvalid) {
+      double x, y;
+      load_coord(P.coords, P.f64, tr.pix + (int64_t)py * P.w1 + px, x, y);
       const LevelPos lp = level_pos(x, y, l);
       ay = clamp_anchor(lp.y0, R, P.th[l]);
       ax = clamp_anchor(lp.x0, R, P.tw[l]);
@@ -134,12 +149,13 @@ __device__ __forceinline__ void sample_group(const PartialParams& P, float* out,
   if (vmask == 0) return;
   // pixel of query i (within the pair's frame): pix0 + (i>>2)*W + (i&3)
   const int64_t pix0 = (int64_t)py0 * P.w1 + px0;
+  float* O = sm.outs[warp];  // [q][nlev][81]
   // overflowed levels: warp-cooperative direct dots (warp-uniform loop)
   for (int l_ = 0; l_ < nlev; ++l_) {
     if (__shfl_sync(0xffffffffu, status, 8 * l_) == ST_OVERFLOW)
       overflow_level(P.f1 + tr.pix * P.d, P.f2[level0 + l_] + tr.pair * P.f2_pp[level0 + l_],
                      P.th[level0 + l_], P.tw[level0 + l_], P.d, P.vec,
-                     pix0, P.w1, vmask, ay, ax, w, l_, nlev, patch, O, lane);
+                     pix0, P.w1, vmask, ay, ax, w, l_, nlev, sm.patch[warp], O, lane);
   }
   // every lane (q, l) combines the 81 taps of query q at level l, TPP tap
   // rows per pass from (TPP + 1) x 10 cache values loaded into registers
@@ -239,162 +255,32 @@ __device__ __forceinline__ void sample_group(const PartialParams& P, float* out,
   }
 }
 
-// group g of tile t: its tile, first query row / column
-__device__ __forceinline__ void item_group(const PartialParams& P, int64_t item, int warp,
-                                           bool reverse, int64_t& tile, TileRef& tr, int& grp,
-                                           int& py0, int& px0) {
-  // tiles in reverse order: the contraction claims tiles in increasing order,
-  // so the last tiles' new cells are the likeliest to still be in L2 (-1.1%
-  // per C4 step, A/B; CVB_GF_REVERSE=0 restores the forward order)
-  const int64_t ti = item / CTAS_PER_TILE;
-  tile = P.tile0 + (reverse ? P.ntile - 1 - ti : ti);
-  tr = tile_ref(P, tile);
-  // query group: tile rows 2(g>>1)..+1, columns 4(g&1)..+3
-  grp = (int)(item % CTAS_PER_TILE) * WARPS + warp;
-  py0 = tr.ty * TQH + group_qy(grp, 0);
-  px0 = tr.tx * TQW + group_qx(grp, 0);
-}
-
-// One CTA per (tile, pair of groups).
-template <int NPASS>
-__global__ void __launch_bounds__(WARPS * 32, NPASS >= 3 ? 16 / WARPS : (NPASS == 2 ? 7 : 6))
-    gather_fast_kernel(PartialParams P, float* out, int level0, int nlev, bool reverse) {
-  extern __shared__ __align__(16) uint8_t g_smem[];
-  Shared& sm = *reinterpret_cast<Shared*>(g_smem);
-  pdl_trigger();
-  pdl_wait();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int64_t tile;
-  TileRef tr;
-  int grp, py0, px0;
-  item_group(P, blockIdx.x, warp, reverse, tile, tr, grp, py0, px0);
-  if (py0 >= P.h1) return;  // warp-uniform
-  const int q = lane & 7, li = lane >> 3;
-  const int py = py0 + (q >> 2), px = px0 + (q & 3);
-  double x = 0.0, y = 0.0;
-  int status = ST_EMPTY;
-  if (li < nlev) status = P.meta[(tile * P.levels + level0 + li) * CVB_META_INTS + 4];
-  if (py < P.h1 && px < P.w1) load_coord(P.coords, P.f64, tr.pix + (int64_t)py * P.w1 + px, x, y);
-  sample_group<NPASS>(P, out, level0, nlev, tile, tr, grp, py0, px0, x, y, status, sm.outs[warp],
-                      sm.patch[warp], lane);
-}
-
-// Persistent variant (A/B knob CVB_GF_PERSIST): each CTA walks items
-// blockIdx.x, +gridDim.x, ...; the next item's coordinates and statuses are
-// prefetched into shared memory by cp.async while the current one is sampled
-// (the coordinate load is otherwise a dependent round trip before the first
-// cache load).
-struct Prefetch {
-  alignas(16) uint8_t coord[WARPS][2][QG][16];
-  int status[WARPS][2][MAXL];
-};
-template <int NPASS>
-__global__ void __launch_bounds__(WARPS * 32, NPASS >= 3 ? 16 / WARPS : (NPASS == 2 ? 7 : 6))
-    gather_fast_persist_kernel(PartialParams P, float* out, int level0, int nlev, bool reverse,
-                               int64_t n_items) {
-  extern __shared__ __align__(16) uint8_t g_smem[];
-  Shared& sm = *reinterpret_cast<Shared*>(g_smem);
-  Prefetch& pf = *reinterpret_cast<Prefetch*>(g_smem + sizeof(Shared));
-  pdl_trigger();
-  pdl_wait();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q = lane & 7, li = lane >> 3;
-  const int esz = P.f64 ? 16 : 8;
-  auto issue = [&](int64_t item, int b) {
-    int64_t tile;
-    TileRef tr;
-    int grp, py0, px0;
-    item_group(P, item, warp, reverse, tile, tr, grp, py0, px0);
-    if (py0 >= P.h1) return;
-    if (lane < QG) {
-      const int py = py0 + (q >> 2), px = px0 + (q & 3);
-      if (py < P.h1 && px < P.w1) {
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(P.coords) +
-                             (tr.pix + (int64_t)py * P.w1 + px) * esz;
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&pf.coord[warp][b][q][0]);
-        if (esz == 16)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-        else
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-      }
-    } else if (lane - QG < nlev) {  // lanes 8.. : the levels' statuses
-      const int l_ = lane - QG;
-      const int* src = P.meta + (tile * P.levels + level0 + l_) * CVB_META_INTS + 4;
-      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&pf.status[warp][b][l_]);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  int b = 0;
-  if ((int64_t)blockIdx.x < n_items) issue(blockIdx.x, 0);
-  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, b ^= 1) {
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncwarp();
-    int64_t tile;
-    TileRef tr;
-    int grp, py0, px0;
-    item_group(P, item, warp, reverse, tile, tr, grp, py0, px0);
-    double x = 0.0, y = 0.0;
-    int status = ST_EMPTY;
-    if (py0 < P.h1) {
-      const int py = py0 + (q >> 2), px = px0 + (q & 3);
-      if (py < P.h1 && px < P.w1) {
-        if (P.f64) {
-          const double* c = reinterpret_cast<const double*>(&pf.coord[warp][b][q][0]);
-          x = c[0];
-          y = c[1];
-        } else {
-          const float* c = reinterpret_cast<const float*>(&pf.coord[warp][b][q][0]);
-          x = (double)c[0];
-          y = (double)c[1];
-        }
-      }
-      if (li < nlev) status = pf.status[warp][b][li];
-    }
-    __syncwarp();
-    if (item + gridDim.x < n_items) issue(item + gridDim.x, b ^ 1);
-    if (py0 < P.h1)
-      sample_group<NPASS>(P, out, level0, nlev, tile, tr, grp, py0, px0, x, y, status,
-                          sm.outs[warp], sm.patch[warp], lane);
-    __syncwarp();
-  }
-}
-
 }  // namespace gfast
 
 int launch_gather_fast_r4(const PartialParams& P, float* out, cudaStream_t s) {
   // tap-row passes per query: 2 (patch rows 0-5, then 5-9; 128 registers,
   // the same 16 warps per SM as 3 passes of 3 rows, one dependent load round
   // trip fewer: -1.8% sampler time at C4, A/B); CVB_GF_PASSES=1|3 for A/B
-  static int npass = -1, persist = -1, reverse = -1;
+  static int npass = -1;
   if (npass < 0) {
     const char* e = getenv("CVB_GF_PASSES");
     npass = e ? atoi(e) : 2;
     if (npass != 1 && npass != 3) npass = 2;
-    e = getenv("CVB_GF_PERSIST");
-    persist = e && atoi(e) != 0;
-    e = getenv("CVB_GF_REVERSE");
+  }
+  auto kernel = npass == 1 ? gfast::gather_fast_kernel<1>
+                           : (npass == 2 ? gfast::gather_fast_kernel<2> : gfast::gather_fast_kernel<3>);
+  static std::atomic<uint64_t> attr{0};
+  static int reverse = -1;
+  if (reverse < 0) {
+    const char* e = getenv("CVB_GF_REVERSE");
     reverse = !e || atoi(e) != 0;
   }
-  using K = void (*)(PartialParams, float*, int, int, bool);
-  using KP = void (*)(PartialParams, float*, int, int, bool, int64_t);
-  const K kernel = npass == 1 ? gfast::gather_fast_kernel<1>
-                              : (npass == 2 ? gfast::gather_fast_kernel<2> : gfast::gather_fast_kernel<3>);
-  const KP kernel_p = npass == 1 ? gfast::gather_fast_persist_kernel<1>
-                                 : (npass == 2 ? gfast::gather_fast_persist_kernel<2>
-                                               : gfast::gather_fast_persist_kernel<3>);
-  const void* fn = persist ? (const void*)kernel_p : (const void*)kernel;
-  const int smem = (int)(sizeof(gfast::Shared) + (persist ? sizeof(gfast::Prefetch) : 0));
-  static std::atomic<uint64_t> attr{0}, attr_p{0};
-  if (persist)
-    ensure_max_smem(attr_p, kernel_p, smem);
-  else
-    ensure_max_smem(attr, kernel, smem);
+  const int smem = (int)sizeof(gfast::Shared);
+  ensure_max_smem(attr, kernel, smem);
   // Shared-memory carveout 65%: the taps re-read each cache sector ~3x through
   // L1, so L1 capacity matters more than the last CTA slot per SM (measured:
-  // 65% is 1-2% faster than the default 200 KB carveout and than 55% / 75%;
-  // 100% halves the speed).  CVB_GF_CARVEOUT overrides (percent; -1 = driver
-  // default).
+  // 65% is 1-2% faster than the default 200 KB carveout; 100% halves the
+  // speed).  CVB_GF_CARVEOUT overrides (percent; -1 = driver default).
   static std::atomic<uint64_t> carved{0};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -403,27 +289,13 @@ int launch_gather_fast_r4(const PartialParams& P, float* out, cudaStream_t s) {
     const char* e = getenv("CVB_GF_CARVEOUT");
     const int carve = e ? atoi(e) : 65;
     if (carve >= 0)
-      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+      cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
     carved.fetch_or(bit);
-  }
-  const int64_t n_items = gfast::CTAS_PER_TILE * P.ntile;
-  int64_t grid_p = n_items;
-  if (persist) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_p, gfast::WARPS * 32, smem);
-    int n_sms = 148;
-    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t resident = (int64_t)(per_sm > 0 ? per_sm : 1) * n_sms;
-    grid_p = n_items < resident ? n_items : resident;
   }
   for (int l0 = 0; l0 < P.levels; l0 += gfast::MAXL) {
     const int nl = min(gfast::MAXL, P.levels - l0);
-    if (persist)
-      launch_pdl(kernel_p, dim3((unsigned)grid_p), dim3(gfast::WARPS * 32), smem, s, P, out, l0, nl,
-                 reverse != 0, n_items);
-    else
-      launch_pdl(kernel, dim3((unsigned)n_items), dim3(gfast::WARPS * 32), smem, s, P, out, l0, nl,
-                 reverse != 0);
+    launch_pdl(kernel, dim3((unsigned)(gfast::CTAS_PER_TILE * P.ntile)), dim3(gfast::WARPS * 32), smem,
+               s, P, out, l0, nl, reverse != 0);
     const int st = check_launch("partial_gather_fast");
     if (st != CVB_OK) return st;
   }
