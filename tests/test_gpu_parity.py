@@ -411,6 +411,54 @@ def test_more_levels_than_one_sampler_launch(cuda, levels, radius):
         assert dev <= REF_GATE and ns <= NS_GATE
 
 
+@pytest.mark.parametrize("split", ["row_aligned", "mid_row"])
+def test_disjoint_ranges_contract_concurrently(cuda, split):
+    """include/corrvol_b200.h: disjoint tile ranges may run concurrently.  Two
+    ranges contracted and gathered on two streams at once, every iteration
+    (a mid-row split also puts the cold iteration on the single-tile kernel
+    instead of the SM pairs) == one launch over the frame, bit for bit."""
+    from paper_2505_16942_b200 import _lib, sparse
+    from paper_2505_16942_b200.dense import coords_flags
+    spec = cvb.LookupSpec(4, 4)
+    sc = cvb.gen_scenario(6, (72, 104, 64), 5, spec, coords_dtype=np.float32)
+    f1 = cvb.FeatureMap(torch.from_numpy(sc.f1).to(cuda))
+    f2 = cvb.FeatureMap(torch.from_numpy(sc.f2).to(cuda))
+    ref = cvb.init_state(f1, f2, spec)
+    st = cvb.init_state(f1, f2, spec)
+    n, tx = st.n_tiles, -(-104 // 8)
+    k = (n // tx // 2) * tx if split == "row_aligned" else n // 2 + 3
+    full = st.desc
+    ranges = []
+    for a, b in ((0, k), (k, n)):
+        d = _lib.PartialDesc()
+        _lib.C.pointer(d)[0] = full
+        d.tile_begin, d.tile_end = a, b
+        ranges.append(d)
+    streams = [torch.cuda.Stream(cuda), torch.cuda.Stream(cuda)]
+    main = torch.cuda.current_stream(cuda)
+    for coords in sc.centroid_fields:
+        c = cvb.CentroidField(torch.from_numpy(coords).to(cuda))
+        want = cvb.sample_iteration(ref, c).numpy()
+        out = torch.empty((72, 104, 4, 9, 9), dtype=torch.float32, device=cuda)
+        flags = coords_flags(c, False)
+        f2s, caches = sparse._contract_args(st, c, flags)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        try:
+            for d, s in zip(ranges, streams):
+                s.wait_event(ev)
+                with torch.cuda.stream(s):
+                    st.desc = d
+                    sparse._contract(st, c, flags, f2s, caches)
+                    sparse._gather(st, c, flags, f2s, caches, out)
+        finally:
+            st.desc = full
+        for s in streams:
+            main.wait_stream(s)
+        st.iteration += 1
+        assert np.array_equal(out.cpu().numpy(), want)
+
+
 def test_tc_per_row_scaling_wide_dynamic_range(cuda):
     """Rows spanning 2^-20 .. 2^20 in magnitude: every row carries its own
     power-of-two scale through the fp16 split, so both gates hold per row."""
