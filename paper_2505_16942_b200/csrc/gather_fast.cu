@@ -259,8 +259,8 @@ __global__ void __launch_bounds__(WARPS * 32, NPASS >= 3 ? 16 / WARPS : (NPASS =
 
 int launch_gather_fast_r4(const PartialParams& P, float* out, cudaStream_t s) {
   // tap-row passes per query: 2 (patch rows 0-5, then 5-9; 128 registers,
-  // the same 16 warps per SM as 3 passes of 3 rows, one dependent load round
-  // trip fewer: -1.8% sampler time at C4, A/B); CVB_GF_PASSES=1|3 for A/B
+  // the occupancy of 3 passes of 3 rows, one dependent load round trip
+  // fewer: -1.8% sampler time at C4, A/B); CVB_GF_PASSES=1|3 for A/B
   static int npass = -1;
   if (npass < 0) {
     const char* e = getenv("CVB_GF_PASSES");
