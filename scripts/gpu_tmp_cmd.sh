@@ -1,7 +1,7 @@
-for v in 3 2 1; do CVB_GF_PASSES=$v python scripts/dbg/out_hash.py C4 | sed "s/^/passes=$v /"; done
-for rep in 1 2 3; do for v in 3 2 1; do
-  CVB_GF_PASSES=$v timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-compare > gpurun_out/ab.json 2>gpurun_out/ab.err
+for v in 0 1 2 3; do CVB_GF_HINT=$v python scripts/dbg/out_hash.py C4 | sed "s/^/hint=$v /"; done
+for rep in 1 2 3; do for v in 0 1 2 3; do
+  CVB_GF_HINT=$v timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-compare > gpurun_out/ab.json 2>gpurun_out/ab.err
   python -c "
 import json,statistics; d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1]); k=d['kernel_ms']
-print('passes=$v', d['value'], 'contract it0 %.3f warm %.4f gather %.4f' % (k['contract_ms'][0], statistics.mean(k['contract_ms'][1:]), statistics.mean(k['gather_ms'][1:])))" || tail -3 gpurun_out/ab.err
+print('hint=$v', d['value'], 'contract it0 %.3f warm %.4f gather %.4f' % (k['contract_ms'][0], statistics.mean(k['contract_ms'][1:]), statistics.mean(k['gather_ms'][1:])))" || tail -3 gpurun_out/ab.err
 done; done
