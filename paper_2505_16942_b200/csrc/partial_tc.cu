@@ -920,31 +920,37 @@ __global__ void __launch_bounds__(PLAN_WARPS * 32) plan_kernel(PartialParams P) 
 #pragma unroll
       for (int i = 0; i < 5; ++i) pm[i] = meta[i];
     }
-    int mylo_y = 0, myhi_y = 0, mylo_x = 0, myhi_x = 0;  // lane l keeps level l
-    for (int l = 0; l < P.levels; ++l) {
-      int ylo = INT_MAX, yhi = INT_MIN, xlo = INT_MAX, xhi = INT_MIN;
+    // Level floors from the level-0 floor: floor(x / 2^l) == floor(x) >> l
+    // (x * 2^-l is exact in fp64), and shifting and clamp_anchor are both
+    // monotonic, so the tile's per-level anchor range is the shifted, clamped
+    // range of its level-0 floors — one fp64 floor per coordinate and one
+    // warp reduction for all levels.  Floors are saturated to +-2^30 first
+    // (beyond any grid: they clamp to the same anchors at every level).
+    int fxlo = INT_MAX, fxhi = INT_MIN, fylo = INT_MAX, fyhi = INT_MIN;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (v[h]) {
-          const LevelPos lp = level_pos(x[h], y[h], l);
-          const int ay = clamp_anchor(lp.y0, r, P.th[l]), ax = clamp_anchor(lp.x0, r, P.tw[l]);
-          ylo = min(ylo, ay);
-          yhi = max(yhi, ay);
-          xlo = min(xlo, ax);
-          xhi = max(xhi, ax);
-        }
+    for (int h = 0; h < 2; ++h) {
+      if (v[h]) {
+        const LevelPos lp = level_pos(x[h], y[h], 0);
+        const long long sat = 1ll << 30;
+        const int fx = (int)(lp.x0 < -sat ? -sat : (lp.x0 > sat ? sat : lp.x0));
+        const int fy = (int)(lp.y0 < -sat ? -sat : (lp.y0 > sat ? sat : lp.y0));
+        fxlo = min(fxlo, fx);
+        fxhi = max(fxhi, fx);
+        fylo = min(fylo, fy);
+        fyhi = max(fyhi, fy);
       }
-      // warp reductions in one redux.sync each
-      ylo = __reduce_min_sync(0xffffffffu, ylo);
-      yhi = __reduce_max_sync(0xffffffffu, yhi);
-      xlo = __reduce_min_sync(0xffffffffu, xlo);
-      xhi = __reduce_max_sync(0xffffffffu, xhi);
-      if (lane == l) {
-        mylo_y = ylo;
-        myhi_y = yhi;
-        mylo_x = xlo;
-        myhi_x = xhi;
-      }
+    }
+    fxlo = __reduce_min_sync(0xffffffffu, fxlo);
+    fxhi = __reduce_max_sync(0xffffffffu, fxhi);
+    fylo = __reduce_min_sync(0xffffffffu, fylo);
+    fyhi = __reduce_max_sync(0xffffffffu, fyhi);
+    int mylo_y = 0, myhi_y = 0, mylo_x = 0, myhi_x = 0;  // lane l: level l's anchor range
+    if (lane < P.levels && nv > 0) {
+      const int l = lane;
+      mylo_y = clamp_anchor(fylo >> l, r, P.th[l]);
+      myhi_y = clamp_anchor(fyhi >> l, r, P.th[l]);
+      mylo_x = clamp_anchor(fxlo >> l, r, P.tw[l]);
+      myhi_x = clamp_anchor(fxhi >> l, r, P.tw[l]);
     }
     int n_new = 0;
     unsigned long long c_ovf = 0, c_empty = 0, c_dots, c_cells;

@@ -1,7 +1,4 @@
-for v in 0 1 2 3; do CVB_GF_HINT=$v python scripts/dbg/out_hash.py C4 | sed "s/^/hint=$v /"; done
-for rep in 1 2 3; do for v in 0 1 2 3; do
-  CVB_GF_HINT=$v timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-compare > gpurun_out/ab.json 2>gpurun_out/ab.err
-  python -c "
-import json,statistics; d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1]); k=d['kernel_ms']
-print('hint=$v', d['value'], 'contract it0 %.3f warm %.4f gather %.4f' % (k['contract_ms'][0], statistics.mean(k['contract_ms'][1:]), statistics.mean(k['gather_ms'][1:])))" || tail -3 gpurun_out/ab.err
-done; done
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_plan.log 2>&1; echo pytest rc $?; tail -2 gpurun_out/pytest_plan.log
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:plan_kernel --csv python bench.py --profile-only --steps 1 --warmup 0 > gpurun_out/plan_ncu.csv 2>&1
+grep gpu__time gpurun_out/plan_ncu.csv | awk -F'","' '{print $NF}' | tr -d '"' | tail -12 | tr '\n' ' '; echo
+bash scripts/gpu_ab.sh 3
