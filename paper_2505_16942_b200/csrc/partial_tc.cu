@@ -466,8 +466,11 @@ constexpr int NBP = CVB_TC_NBP;     // F1 pieces in the ring (16 KB each)
 #define CVB_TC_NPL 3  // plan slots: 3 is 1.7% faster warm than 4 (A/B, round 2)
 #endif
 constexpr int NPL = CVB_TC_NPL;     // plan slots
-constexpr int THREADS = 512;
-constexpr int A_WARPS = 8;             // A producers: warps 4-7 and 12-15
+#ifndef CVB_TC_AW
+#define CVB_TC_AW 8
+#endif
+constexpr int A_WARPS = CVB_TC_AW;     // A producers: warps 4-7 (and 12-15 when 8)
+constexpr int THREADS = A_WARPS == 8 ? 512 : 384;
 constexpr int A_ROWS = 128 / A_WARPS;  // A rows per producer warp
 // Pipeline watchdog: a ring wait that has not completed after this long
 // (%globaltimer ns) means a broken pipeline, not a slow one.  The CTA then sets
@@ -1141,9 +1144,9 @@ constexpr int NST = CVB_TC2_NST;
 constexpr int NBP = CVB_TC2_NBP;
 constexpr int NPL = CVB_TC2_NPL;
 constexpr int PMAXL = 4;  // levels the pair kernel handles (more: single-tile kernel)
-using tcp::THREADS;
-using tcp::A_WARPS;
-using tcp::A_ROWS;
+constexpr int THREADS = 512;
+constexpr int A_WARPS = 8;             // A producers: warps 4-7 and 12-15
+constexpr int A_ROWS = 128 / A_WARPS;
 
 constexpr int M2 = 256;  // cells per pair chunk (128 per CTA)
 // accumulators: main (hi.hi) and corr (hi.lo + lo.hi) in 128 TMEM columns
@@ -1874,7 +1877,7 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
     ensure_max_smem(dbg ? attr2_dbg : attr2, kernel2, (int)smem2);
     const int64_t max_cl = n_sms / 2;
     const int64_t grid2 = 2 * (n_pairs < max_cl ? n_pairs : max_cl);
-    launch_pdl(kernel2, dim3((unsigned)grid2), dim3(tcp::THREADS), smem2,
+    launch_pdl(kernel2, dim3((unsigned)grid2), dim3(tcp2::THREADS), smem2,
                as_stream(stream), T, n_pairs);
     return check_launch("partial_contract_tcp2");
   }
