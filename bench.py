@@ -23,9 +23,11 @@ import os
 import statistics
 import subprocess
 import sys
+import shutil
 import tempfile
 import time
 from pathlib import Path
+from typing import Optional
 
 import numpy as np
 
@@ -66,6 +68,7 @@ def parse():
     ap.add_argument("--profile-only", action="store_true",
                     help="run warmup+steps only (for ncu); print nothing else")
     ap.add_argument("--cpu-baseline-worker", default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--parity-dir", default=None, help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -217,7 +220,20 @@ def host_info() -> dict:
     return info
 
 
-def _ref_variant_times(cfg: str) -> dict:
+PARITY_ROWS = 16  # rows of the timed reference band checked against the GPU
+
+
+def _partial_band(cfg: str):
+    """Rows the CPU-baseline worker times the reference partial sampler on:
+    the whole frame at C1, else a 32-row band of whole tiles mid-frame."""
+    h = CONFIGS[cfg][0]
+    if cfg == "C1":
+        return 0, h
+    a = h // 2 // 8 * 8
+    return a, a + 32
+
+
+def _ref_variant_times(cfg: str, parity_dir: Optional[str] = None) -> dict:
     """The reference's three samplers on ONE core (harness.py:304-437):
     full runs at C1; at larger configs the partial sampler on a 32-row band
     (all iterations) and on-demand on an 8-row band (first 2 iterations), both
@@ -236,19 +252,47 @@ def _ref_variant_times(cfg: str) -> dict:
     full = cfg == "C1"
     res = {}
     # partial
-    a, b = (0, h) if full else (h // 2 // 8 * 8, h // 2 // 8 * 8 + 32)
+    a, b = _partial_band(cfg)
     f1 = cv.FeatureMap(values=sc.f1[a:b])
     f2 = cv.FeatureMap(values=sc.f2)
+    # the GPU's outputs for the first PARITY_ROWS rows of this band (fast and
+    # strict arithmetic, every iteration), written by the B200 arm: the
+    # reference's own outputs check them here, outside the timed calls
+    fast = strict = None
+    if parity_dir is not None:
+        fast = np.load(os.path.join(parity_dir, "fast.npy"), mmap_mode="r")
+        strict = np.load(os.path.join(parity_dir, "strict.npy"), mmap_mode="r")
+    pr = min(PARITY_ROWS, b - a)
+    n1 = float(np.sqrt((sc.f1[a:a + pr].astype(np.float64) ** 2).sum(-1)).max())
+    n2 = float(np.sqrt((sc.f2.astype(np.float64) ** 2).sum(-1)).max())
+    dev = ns = 0.0
+    bitwise = True
     t0 = time.perf_counter()
     st = cv.init_state(f1, f2, spec, 8, backend="cython")
     t1 = time.perf_counter()
-    for c in cents:
-        cv.sample_iteration(st, cv.CentroidField(coords=c[a:b]))
+    t_it = 0.0
+    for i, c in enumerate(cents):
+        tq = time.perf_counter()
+        cm = cv.sample_iteration(st, cv.CentroidField(coords=c[a:b]))
+        t_it += time.perf_counter() - tq
+        if fast is not None:
+            want = np.asarray(cm.values)[:pr]
+            d = float(np.abs(np.asarray(fast[i]) - want).max())
+            dev = max(dev, d / (1.0 + float(np.abs(want).max())))
+            ns = max(ns, d / max(n1 * n2, 1e-30))
+            bitwise = bitwise and np.array_equal(np.asarray(strict[i]), want)
     t2 = time.perf_counter()
-    frame_s = (t1 - t0) + (t2 - t1) * h / (b - a)
+    frame_s = (t1 - t0) + t_it * h / (b - a)
     res["partial"] = {"ms_per_iter": 1e3 * frame_s / n_iter, "rows": [a, b],
-                      "iterations": n_iter, "measured_s": t2 - t0,
+                      "iterations": n_iter, "measured_s": (t1 - t0) + t_it,
                       "extrapolated": not full}
+    if fast is not None:
+        res["parity"] = {"checker": "reference corrvol 0.1.0 partial sampler (the timed band)",
+                         "rows": [a, a + pr], "iterations": n_iter,
+                         "fast_ref_gate": dev, "fast_ns_gate": ns,
+                         "strict_bitwise": bool(bitwise),
+                         "gates": {"ref": 1e-5, "ns": 1e-4},
+                         "pass": bool(bitwise and dev <= 1e-5 and ns <= 1e-4)}
     # on-demand
     a, b = (0, h) if full else (h // 2 // 8 * 8, h // 2 // 8 * 8 + 8)
     its = n_iter if full else 2
@@ -281,8 +325,8 @@ def _ref_variant_times(cfg: str) -> dict:
     return res
 
 
-def cpu_baseline_worker(cfg: str) -> None:
-    print(json.dumps(_ref_variant_times(cfg)))
+def cpu_baseline_worker(cfg: str, parity_dir: Optional[str] = None) -> None:
+    print(json.dumps(_ref_variant_times(cfg, parity_dir)))
 
 
 def _ref_cores(cfg: str) -> int:
@@ -347,15 +391,42 @@ def run_reference_arm(args) -> None:
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(cfg: str) -> dict:
+def _parity_outputs(cvb, torch, f1_dev, f2_dev, cents, spec, cfg: str, pdir: str) -> None:
+    """The GPU's cost maps on the rows the CPU-baseline worker's reference band
+    starts with (_partial_band): fast arithmetic from a full-frame sampler,
+    strict from a sampler on the band's rows (row bands of whole 8-row tiles
+    are exact), every iteration; saved for the worker to check."""
+    a, ref_b = _partial_band(cfg)
+    b = min(ref_b, a + PARITY_ROWS)
+    fast = cvb.CorrSampler(cvb.FeatureMap(f1_dev, check=False), cvb.FeatureMap(f2_dev, check=False),
+                           spec, check=False)
+    strict = cvb.CorrSampler(cvb.FeatureMap(f1_dev[a:ref_b].contiguous(), check=False),
+                             cvb.FeatureMap(f2_dev, check=False), spec, strict=True, check=False)
+    got_f, got_s = [], []
+    for c in cents:
+        got_f.append(fast(c).values[a:b].cpu().numpy())
+        band = cvb.CentroidField(c.coords[a:ref_b].contiguous(), check=False)
+        got_s.append(strict(band).values[:b - a].cpu().numpy())
+    np.save(os.path.join(pdir, "fast.npy"), np.stack(got_f))
+    np.save(os.path.join(pdir, "strict.npy"), np.stack(got_s))
+    del fast, strict
+    torch.cuda.empty_cache()
+
+
+def cpu_baseline(cfg: str, parity_dir: Optional[str] = None) -> dict:
     """`cpu_baseline` of the B200 arm: the reference's dense, on-demand and
     partial samplers timed on ONE host core (taskset -c 0) in a subprocess;
-    `value` is the partial sampler (the path this build replaces)."""
+    `value` is the partial sampler (the path this build replaces).  With
+    `parity_dir` the reference's partial outputs also check the GPU's on the
+    first rows of its band (returned under "parity", popped by the caller)."""
     try:
-        res = subprocess.run(["taskset", "-c", "0", sys.executable, str(ROOT / "bench.py"),
-                              "--cpu-baseline-worker", cfg],
-                             capture_output=True, text=True, timeout=900)
+        cmd = ["taskset", "-c", "0", sys.executable, str(ROOT / "bench.py"),
+               "--cpu-baseline-worker", cfg]
+        if parity_dir is not None:
+            cmd += ["--parity-dir", parity_dir]
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
         ref = json.loads(res.stdout.strip().splitlines()[-1])
+        parity = ref.pop("parity", None)
         p = ref["partial"]
         parts = []
         for name in ("partial", "ondemand", "dense"):
@@ -372,7 +443,7 @@ def cpu_baseline(cfg: str) -> dict:
                           f"{cfg}: " + "; ".join(parts),
                 "variants": {k: {kk: (round(vv, 3) if isinstance(vv, float) else vv)
                                  for kk, vv in v.items()} for k, v in ref.items()},
-                "host": host_info()}
+                "host": host_info(), "parity": parity}
     except Exception as exc:  # report, never fake
         return {"value": None, "unit": "ms/iter", "cores": 1, "kind": "reference",
                 "sample": f"failed: {type(exc).__name__}: {exc}"[:300]}
@@ -438,7 +509,7 @@ class Clocks:
 def main():
     args = parse()
     if args.cpu_baseline_worker:
-        cpu_baseline_worker(args.cpu_baseline_worker)
+        cpu_baseline_worker(args.cpu_baseline_worker, args.parity_dir)
         return
     if args.impl == "reference":
         run_reference_arm(args)
@@ -728,8 +799,16 @@ def main():
 
     # ---- CPU baseline (rank 0, N=1) ----------------------------------------
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.config)
+        pdir = None
+        if args.variant == "partial" and not args.strict:
+            pdir = tempfile.mkdtemp(prefix="cvb_parity_")
+            _parity_outputs(cvb, torch, f1_dev, f2_dev, cents, spec, args.config, pdir)
+        cpu = cpu_baseline(args.config, pdir)
+        parity = cpu.pop("parity", None)
+        if pdir is not None:
+            shutil.rmtree(pdir, ignore_errors=True)
 
     if rank == 0:
         line = {
@@ -758,7 +837,8 @@ def main():
             "tensor_cores": kern.get("tensor_cores") if kern else None,
             "device_counters": kern.get("device_counters") if kern else None,
             "compare": compare or None,
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
+            "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "clocks": clk,
+            "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

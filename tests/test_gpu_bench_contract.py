@@ -51,3 +51,16 @@ def test_reference_arm_line(cuda):
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_bench_parity_against_the_reference(cuda):
+    """The CPU-baseline leg's reference run checks the GPU's cost maps on the
+    rows it times (every iteration): strict bitwise, fast within both gates."""
+    if import_reference() is None:
+        pytest.skip("oracle/_ref not built")
+    d = _run("--config", "C1", "--steps", "3", "--warmup", "3", "--no-e2e", "--no-compare",
+             timeout=900)
+    p = d["parity"]
+    assert p["iterations"] == 12 and p["rows"][1] > p["rows"][0]
+    assert p["strict_bitwise"] and p["pass"]
+    assert p["fast_ref_gate"] <= 1e-5 and p["fast_ns_gate"] <= 1e-4
