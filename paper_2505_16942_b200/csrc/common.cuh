@@ -40,11 +40,12 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
-bool pdl_enabled();  // opt-in: CVB_PDL=1
+bool pdl_enabled();    // opt-in: CVB_PDL=1 (every per-iteration edge)
+bool pdl_in_phase();   // default (CVB_PDL unset or 2): the tiler -> contraction -> sampler edges
 
 template <typename... KArgs, typename... Args>
-static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                                     cudaStream_t s, Args&&... args) {
+static inline cudaError_t launch_pdl_if(bool allow, void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                                        size_t smem, cudaStream_t s, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -52,10 +53,22 @@ static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 b
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = allow ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                     cudaStream_t s, Args&&... args) {
+  return launch_pdl_if(pdl_enabled(), kernel, grid, block, smem, s, std::forward<Args>(args)...);
+}
+// a launch that depends on the previous kernel of the same iteration
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl_phase(void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                                           size_t smem, cudaStream_t s, Args&&... args) {
+  return launch_pdl_if(pdl_enabled() || pdl_in_phase(), kernel, grid, block, smem, s,
+                       std::forward<Args>(args)...);
 }
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // image pairs described by a partial-sampler descriptor (0 means 1)

@@ -294,7 +294,7 @@ int launch_gather_fast_r4(const PartialParams& P, float* out, cudaStream_t s) {
   }
   for (int l0 = 0; l0 < P.levels; l0 += gfast::MAXL) {
     const int nl = min(gfast::MAXL, P.levels - l0);
-    launch_pdl(kernel, dim3((unsigned)(gfast::CTAS_PER_TILE * P.ntile)), dim3(gfast::WARPS * 32), smem,
+    launch_pdl_phase(kernel, dim3((unsigned)(gfast::CTAS_PER_TILE * P.ntile)), dim3(gfast::WARPS * 32), smem,
                s, P, out, l0, nl, reverse != 0);
     const int st = check_launch("partial_gather_fast");
     if (st != CVB_OK) return st;

@@ -1877,12 +1877,12 @@ int cvb_partial_contract_tc(const cvb_partial_desc* desc, const float* f1,
     ensure_max_smem(dbg ? attr2_dbg : attr2, kernel2, (int)smem2);
     const int64_t max_cl = n_sms / 2;
     const int64_t grid2 = 2 * (n_pairs < max_cl ? n_pairs : max_cl);
-    launch_pdl(kernel2, dim3((unsigned)grid2), dim3(tcp2::THREADS), smem2,
+    launch_pdl_phase(kernel2, dim3((unsigned)grid2), dim3(tcp2::THREADS), smem2,
                as_stream(stream), T, n_pairs);
     return check_launch("partial_contract_tcp2");
   }
   const int64_t grid = T.P.ntile < n_sms ? T.P.ntile : n_sms;
-  launch_pdl(kernel, dim3((unsigned)grid), dim3(tcp::THREADS), smem, as_stream(stream), T);
+  launch_pdl_phase(kernel, dim3((unsigned)grid), dim3(tcp::THREADS), smem, as_stream(stream), T);
   if (T.ts != nullptr) {  // debug timeline dump (CTA 0..3, first 64 tiles, 32 events), ns
     static unsigned long long h[4 * 64 * 32];
     cudaStreamSynchronize(as_stream(stream));

@@ -1,7 +1,8 @@
 """Opt-in launch paths read once per process from the environment, each run
 in a fresh interpreter and compared with the default path of this process:
-  * CVB_PDL=1 — programmatic dependent launch of the per-iteration kernels
-    (csrc/common.cu): outputs bit-identical to plain stream-ordered launches;
+  * CVB_PDL=1 — programmatic dependent launch on every per-iteration edge
+    (csrc/common.cu; the default uses it within an iteration only) and
+    CVB_PDL=0 — plain stream-ordered launches: outputs bit-identical;
   * CVB_TC_DEBUG=16 — the contraction's role timeline (debug only): same
     outputs, and the dump file is written.
 """
@@ -59,6 +60,8 @@ def _run(tmp_path, env_extra):
 def test_pdl_launches_bit_identical(cuda, tmp_path):
     want = _default_outputs(cuda)
     got = _run(tmp_path, {"CVB_PDL": "1"})
+    assert np.array_equal(got, want)
+    got = _run(tmp_path, {"CVB_PDL": "0"})
     assert np.array_equal(got, want)
 
 
