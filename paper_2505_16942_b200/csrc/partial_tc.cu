@@ -487,6 +487,7 @@ struct Ctl {
   uint64_t acc_full[2], acc_empty[2];
   PlanRec slot[NPL];
   alignas(16) int8_t e1[NPL][tc::N];  // the slot's tile's query exponents (bulk-copied with the plan)
+  float qscale[tc::N];                 // dense instantiation: 2^-e_q of the current tile
   uint32_t tmem;
   int abort;  // watchdog fired in this CTA
 };
@@ -703,12 +704,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       // dynamic tile scheduler; the next tile is claimed one record ahead, so
       // the atomic's round trip overlaps the wait for a free slot
-      int64_t t_next = atomicAdd(tile_counter(P), 1);
+      // (only with many tiles per CTA: a tile claimed ahead is one the CTA
+      // cannot give up, which unbalances the tail of short ranges — C2: +3%)
+      const bool ahead = P.ntile >= 16 * (int64_t)gridDim.x;
+      int64_t t_next = ahead ? atomicAdd(tile_counter(P), 1) : 0;
       for (int64_t it = 0;; ++it) {
         const int s = (int)(it % NPL);
         if (!WAIT_EMPTY(U(C.plan_empty[s]), (uint32_t)(it / NPL))) goto done;
+        if (!ahead) t_next = atomicAdd(tile_counter(P), 1);
         const int64_t t = t_next;
-        if (t < P.ntile) t_next = atomicAdd(tile_counter(P), 1);
+        if (ahead && t < P.ntile) t_next = atomicAdd(tile_counter(P), 1);
         if (t >= P.ntile) {  // end of the work list: a sentinel record
           C.slot[s].tile = -1;
           arrive(U(C.plan_full[s]));
@@ -803,6 +808,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int64_t pair = P.batch > 1 ? tile / P.tiles_pp : 0;
       const TileRef tr = DENSE ? tile_ref(P, tile) : TileRef{0, 0, 0, 0};
       const int8_t* e_q = C.e1[s];  // query exponents: scale 2^-(e_q + e_c), exact
+      if (DENSE && n_chunks > 0) {
+        // dense tiles run hundreds of chunks: their 64 query scales as floats
+        // once per tile (the per-element integer scale cost 2.3x in the dense
+        // epilogue's store loop)
+        tc::named_bar(1, 128);
+        if (ep < tc::N) C.qscale[ep] = tc::exp2_neg(e_q[ep]);
+        tc::named_bar(1, 128);
+      }
       for (int c = 0; c < n_chunks; ++c, ++cg) {
         const int ab = cg & 1;
         // the row's cell, cache slot and exponent depend only on the plan:
@@ -853,6 +866,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               tc::st_global_v8(dst + g * plane, o);
             }
           } else if (DENSE && dd != nullptr) {
+            const float s_cd = tc::exp2_neg(e_c);
             // dense rows: query q of the tile -> pixel (8ty + q/8, 8tx + q%8); a
             // warp's lanes are consecutive cells, so each store is 128 B
 #pragma unroll 4
@@ -861,7 +875,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               const int py = tr.ty * TQH + (q >> 3), px = tr.tx * TQW + (q & 7);
               if (py < P.h1 && px < P.w1)
                 dd[((int64_t)py * P.w1 + px) * plane] =
-                    (vm[j] + vc[j]) * tc::exp2_neg(e_q[q] + e_c);
+                    (vm[j] + vc[j]) * (C.qscale[q] * s_cd);
             }
           }
         }
@@ -1425,15 +1439,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       // dynamic pair scheduling: the leader claims pairs (one ahead, so the
       // atomic's round trip overlaps the slot wait) and posts each index into
       // the follower's mailbox for the same slot
-      int64_t pidx_next = leader ? atomicAdd(tcp::tile_counter(P), 1) : 0;  // reset by plan_kernel
+      // (claimed ahead only with many pairs per cluster, as for tiles)
+      const bool ahead = n_pairs >= 8 * (int64_t)gridDim.x;
+      int64_t pidx_next = leader && ahead ? atomicAdd(tcp::tile_counter(P), 1) : 0;  // reset by plan_kernel
       for (int64_t it = 0;; ++it) {
         const int s = (int)(it % NPL);
         if (!WAIT_EMPTY2(U(C.plan_empty[s]), (uint32_t)(it / NPL))) goto done;
         PairSlot& S = C.slot[s];
         int64_t pidx;
         if (leader) {
+          if (!ahead) pidx_next = atomicAdd(tcp::tile_counter(P), 1);
           pidx = pidx_next;
-          if (pidx < n_pairs) pidx_next = atomicAdd(tcp::tile_counter(P), 1);
+          if (ahead && pidx < n_pairs) pidx_next = atomicAdd(tcp::tile_counter(P), 1);
           st_cluster_u64(mapa(tc::smem_u32(&C.pidx[s]), 1), (unsigned long long)pidx);
           asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
                            mapa(U(C.pidx_full[s]), 1))

@@ -1,7 +1,6 @@
-for v in 0 2; do CVB_PDL=$v python scripts/dbg/out_hash.py C4 | sed "s/^/pdl=$v /"; done
-for rep in 1 2 3; do for v in 0 2; do
-  CVB_PDL=$v timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-compare > gpurun_out/ab.json 2>gpurun_out/ab.err
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_dn.log 2>&1; echo pytest rc $?; tail -2 gpurun_out/pytest_dn.log
+for c in C2 C3 C4 C2 C3 C4; do
+  timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ab.json 2>gpurun_out/ab.err
   python -c "
-import json,statistics; d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1]); k=d['kernel_ms']
-print('pdl=$v', d['value'], 'contract it0 %.3f warm %.4f gather %.4f' % (k['contract_ms'][0], statistics.mean(k['contract_ms'][1:]), statistics.mean(k['gather_ms'][1:])))" || tail -3 gpurun_out/ab.err
-done; done
+import json; d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1]); print('$c', d['value'], d['compare'])" || tail -3 gpurun_out/ab.err
+done
