@@ -208,7 +208,7 @@ int cvb_partial_gather(const cvb_partial_desc* desc, const float* f1,
  * and cache as cvb_partial_contract, with the new-cell contraction on
  * tcgen05 (kind::f16, split-fp16 operands, 3 MMAs per K-step, fp32
  * accumulation in TMEM).  cvb_tc_prepare splits F1 (per-tile B-operand
- * images) and every pyramid level (hi/lo planes) once per image pair, each
+ * images) and every pyramid level (hi/lo rows per cell) once per image pair, each
  * row scaled by its own power of two (stored as an exponent byte after the
  * planes); with CVB_PREP_POOL it also produces pyramid levels >= 1 from
  * level 0 (the reference's pool2x2, bit-exact, dense.py:71-86) in the same

@@ -45,6 +45,19 @@ constexpr int A_STAGE = 2 * A_HALF;      // 32 KB
 constexpr int B_HALF = N * KP * 2;       // 8 KB (hi or lo)
 constexpr int B_PIECE = 2 * B_HALF;      // 16 KB
 constexpr int MAX_DP = 256;
+#ifndef CVB_F2_HILO
+#define CVB_F2_HILO 1  // F2 split rows interleaved [cell][hi dp | lo dp]; 0: two planes
+#endif
+// fp16 offsets of cell c's hi row and of its lo row relative to the hi row in
+// a level's split operand.  Interleaved per cell, an A-row fetch's hi and lo
+// 128-byte pieces share a DRAM page (two planes put them ~cells*dp*2 bytes
+// apart): -1% warm contraction, -0.5% per C4 step (A/B)
+__host__ __device__ __forceinline__ int64_t f2_hi(int64_t c, int64_t cells, int dp) {
+  return CVB_F2_HILO ? c * 2 * dp : c * dp;
+}
+__host__ __device__ __forceinline__ int64_t f2_lo_delta(int64_t cells, int dp) {
+  return CVB_F2_HILO ? dp : cells * dp;
+}
 // lo = fp16(x - hi), unscaled: main (hi.hi) + corr (hi.lo + lo.hi) is a plain
 // add in the epilogue
 constexpr int TARGET_EXP = 14;           // max |x * 2^e| < 2^14
@@ -213,7 +226,7 @@ struct TcParams {
   PartialParams P;
   const uint8_t* f1s;                  // per tile: [dp/KP pieces][hi, lo][8 rg][KP/8 kg][8][8] fp16
   const int8_t* e1;                    // per tile: 64 query exponents
-  const __half* f2s[CVB_MAX_LEVELS];   // hi plane [th*tw][dp]; lo = hi + plane
+  const __half* f2s[CVB_MAX_LEVELS];   // per cell: hi row, lo row (f2_hi / f2_lo_delta)
   const int8_t* e2[CVB_MAX_LEVELS];    // per cell exponent
   int64_t plane[CVB_MAX_LEVELS];
   int64_t pair_bytes[CVB_MAX_LEVELS];  // split-operand bytes per pair of the batch, per level
@@ -322,8 +335,8 @@ __device__ __forceinline__ void split_store(const float (&x)[8], int lane, int k
   if (lane < kgs) {
     uint4 hi, lo;
     split8(x, exp2_neg(-e), hi, lo);
-    *reinterpret_cast<uint4*>(planes + c * dp + lane * 8) = hi;
-    *reinterpret_cast<uint4*>(planes + cells * dp + c * dp + lane * 8) = lo;
+    *reinterpret_cast<uint4*>(planes + f2_hi(c, cells, dp) + lane * 8) = hi;
+    *reinterpret_cast<uint4*>(planes + f2_hi(c, cells, dp) + f2_lo_delta(cells, dp) + lane * 8) = lo;
   }
   if (lane == 0) exps[c] = (int8_t)e;
 }
@@ -379,8 +392,8 @@ __global__ void __launch_bounds__(256) split_level_kernel(const float* __restric
     if (lane < kgs) {
       uint4 hi, lo;
       split8(x, exp2_neg(-e), hi, lo);
-      *reinterpret_cast<uint4*>(planes + c * dp + lane * 8) = hi;
-      *reinterpret_cast<uint4*>(planes + cells * dp + c * dp + lane * 8) = lo;
+      *reinterpret_cast<uint4*>(planes + f2_hi(c, cells, dp) + lane * 8) = hi;
+      *reinterpret_cast<uint4*>(planes + f2_hi(c, cells, dp) + f2_lo_delta(cells, dp) + lane * 8) = lo;
     }
     if (lane == 0) exps[c] = (int8_t)e;
   }
@@ -758,8 +771,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           const tc::CellRef cr = tc::cell_of(gi, S.plan, S.prefix, P.levels);
           my_hi = reinterpret_cast<const __half*>(reinterpret_cast<const uint8_t*>(T.f2s[cr.level]) +
                                                   pair * T.pair_bytes[cr.level]) +
-                  ((int64_t)cr.cy * P.tw[cr.level] + cr.cx) * dp;
-          my_plane = T.plane[cr.level];
+                  tc::f2_hi((int64_t)cr.cy * P.tw[cr.level] + cr.cx, 0, dp);
+          my_plane = tc::f2_lo_delta(T.plane[cr.level] / dp, dp);
         }
         for (int kb = 0; kb < n_kb; ++kb, ++g) {
           const int st = (int)(g % NST);
@@ -1535,8 +1548,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const int cy = S.hull[l][0] + idx / S.hw[l], cx = S.hull[l][2] + idx % S.hw[l];
           my_hi = reinterpret_cast<const __half*>(reinterpret_cast<const uint8_t*>(T.f2s[l]) +
                                                   pair * T.pair_bytes[l]) +
-                  ((int64_t)cy * P.tw[l] + cx) * dp;
-          my_plane = T.plane[l];
+                  tc::f2_hi((int64_t)cy * P.tw[l] + cx, 0, dp);
+          my_plane = tc::f2_lo_delta(T.plane[l] / dp, dp);
         }
         for (int kb = 0; kb < n_kb; ++kb, ++g) {
           const int st = (int)(g % NST);
