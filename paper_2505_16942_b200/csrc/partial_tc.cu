@@ -52,7 +52,7 @@ constexpr int MAX_DP = 256;
 // a level's split operand.  Interleaved per cell, an A-row fetch's hi and lo
 // 128-byte pieces share a DRAM page (two planes put them ~cells*dp*2 bytes
 // apart): -1% warm contraction, -0.5% per C4 step (A/B)
-__host__ __device__ __forceinline__ int64_t f2_hi(int64_t c, int64_t cells, int dp) {
+__host__ __device__ __forceinline__ int64_t f2_hi(int64_t c, int dp) {
   return CVB_F2_HILO ? c * 2 * dp : c * dp;
 }
 __host__ __device__ __forceinline__ int64_t f2_lo_delta(int64_t cells, int dp) {
@@ -335,8 +335,8 @@ __device__ __forceinline__ void split_store(const float (&x)[8], int lane, int k
   if (lane < kgs) {
     uint4 hi, lo;
     split8(x, exp2_neg(-e), hi, lo);
-    *reinterpret_cast<uint4*>(planes + f2_hi(c, cells, dp) + lane * 8) = hi;
-    *reinterpret_cast<uint4*>(planes + f2_hi(c, cells, dp) + f2_lo_delta(cells, dp) + lane * 8) = lo;
+    *reinterpret_cast<uint4*>(planes + f2_hi(c, dp) + lane * 8) = hi;
+    *reinterpret_cast<uint4*>(planes + f2_hi(c, dp) + f2_lo_delta(cells, dp) + lane * 8) = lo;
   }
   if (lane == 0) exps[c] = (int8_t)e;
 }
@@ -392,8 +392,8 @@ __global__ void __launch_bounds__(256) split_level_kernel(const float* __restric
     if (lane < kgs) {
       uint4 hi, lo;
       split8(x, exp2_neg(-e), hi, lo);
-      *reinterpret_cast<uint4*>(planes + f2_hi(c, cells, dp) + lane * 8) = hi;
-      *reinterpret_cast<uint4*>(planes + f2_hi(c, cells, dp) + f2_lo_delta(cells, dp) + lane * 8) = lo;
+      *reinterpret_cast<uint4*>(planes + f2_hi(c, dp) + lane * 8) = hi;
+      *reinterpret_cast<uint4*>(planes + f2_hi(c, dp) + f2_lo_delta(cells, dp) + lane * 8) = lo;
     }
     if (lane == 0) exps[c] = (int8_t)e;
   }
@@ -771,7 +771,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           const tc::CellRef cr = tc::cell_of(gi, S.plan, S.prefix, P.levels);
           my_hi = reinterpret_cast<const __half*>(reinterpret_cast<const uint8_t*>(T.f2s[cr.level]) +
                                                   pair * T.pair_bytes[cr.level]) +
-                  tc::f2_hi((int64_t)cr.cy * P.tw[cr.level] + cr.cx, 0, dp);
+                  tc::f2_hi((int64_t)cr.cy * P.tw[cr.level] + cr.cx, dp);
           my_plane = tc::f2_lo_delta(T.plane[cr.level] / dp, dp);
         }
         for (int kb = 0; kb < n_kb; ++kb, ++g) {
@@ -1548,7 +1548,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const int cy = S.hull[l][0] + idx / S.hw[l], cx = S.hull[l][2] + idx % S.hw[l];
           my_hi = reinterpret_cast<const __half*>(reinterpret_cast<const uint8_t*>(T.f2s[l]) +
                                                   pair * T.pair_bytes[l]) +
-                  tc::f2_hi((int64_t)cy * P.tw[l] + cx, 0, dp);
+                  tc::f2_hi((int64_t)cy * P.tw[l] + cx, dp);
           my_plane = tc::f2_lo_delta(T.plane[l] / dp, dp);
         }
         for (int kb = 0; kb < n_kb; ++kb, ++g) {
